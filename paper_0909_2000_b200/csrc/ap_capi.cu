@@ -1,0 +1,665 @@
+// ap_capi.cu — host side of the C ABI (include/alignplot_b200.h).
+//
+// Replaces the reference driver compute_plot (runner.cpp:78-131): validation
+// (model.cpp:46-61) before any device work, then per device: H2D of the raw
+// x slice (rows plus a w-1 halo) and of y, the code-stream
+// kernels (fused $-interleave), the fused comb+extract kernel and either the
+// dense D2H or the deterministic threshold compaction (scoring.cpp:30-39).
+// Rows shard over devices in contiguous blocks; concatenating the blocks in
+// device order is the global row-major order, so the only cross-device step
+// is the gather of per-device hit counts.
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/alignplot_b200.h"
+#include "ap_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? AP_NOMEM : AP_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+    }                                                                                     \
+  } while (0)
+
+// ---- kernel shape table ---------------------------------------------------
+using KernelFn = void (*)(apk::CombParams);
+
+template <int L, int R, bool XM>
+KernelFn pick_fn(bool dense) {
+  return dense ? reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, true, XM>)
+               : reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, false, XM>);
+}
+
+// Table kernels: R in {4, 8, ..., 32}; computed-mask kernels: R in {8, 16, 32}.
+constexpr int kXmRs[] = {8, 16, 32};
+
+template <int L>
+KernelFn pick_r(int R, bool dense, bool xm) {
+  if (xm) {
+    switch (R) {
+      case 8: return pick_fn<L, 8, true>(dense);
+      case 16: return pick_fn<L, 16, true>(dense);
+      case 32: return pick_fn<L, 32, true>(dense);
+    }
+    return nullptr;
+  }
+  switch (R) {
+    case 4: return pick_fn<L, 4, false>(dense);
+    case 8: return pick_fn<L, 8, false>(dense);
+    case 12: return pick_fn<L, 12, false>(dense);
+    case 16: return pick_fn<L, 16, false>(dense);
+    case 20: return pick_fn<L, 20, false>(dense);
+    case 24: return pick_fn<L, 24, false>(dense);
+    case 28: return pick_fn<L, 28, false>(dense);
+    case 32: return pick_fn<L, 32, false>(dense);
+  }
+  return nullptr;
+}
+
+KernelFn pick_kernel(int L, int R, bool dense, bool xm) {
+  switch (L) {
+    case 2: return pick_r<2>(R, dense, xm);
+    case 4: return pick_r<4>(R, dense, xm);
+    case 8: return pick_r<8>(R, dense, xm);
+    case 16: return pick_r<16>(R, dense, xm);
+    case 32: return pick_r<32>(R, dense, xm);
+  }
+  return nullptr;
+}
+
+constexpr size_t kSmemBudget = 200 * 1024;  // per CTA (4 warps)
+
+uint32_t next_pow2(uint32_t v) {
+  uint32_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+struct Shape {
+  int L = 0, R = 0;
+  bool xm = false;   // masks computed in registers (no table)
+  uint32_t ring = 0;
+  size_t smem = 0;
+};
+
+// Cost model per strip pair and column: L lanes x (3 ops per row pair + ~12
+// per-step overhead) + ~25 extraction ops per column.  Feasible shapes must
+// cover W rows and fit the per-warp mismatch table in shared memory.
+bool choose_shape(uint32_t W, uint32_t sigma, Shape* out) {
+  const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
+  double best = 1e30;
+  for (int xm = 0; xm < 2; ++xm) {
+    for (int L : {2, 4, 8, 16, 32}) {
+      for (int R = 4; R <= 32; R += 4) {
+        if (xm && R != 8 && R != 16 && R != 32) continue;
+        if (uint32_t(L * R) < W) continue;
+        if (!xm && uint32_t(L * (R - 4)) >= W && R > 4) continue;  // smaller R covers W
+        const size_t smem =
+            apk::kWarpsPerCta * apk::comb_smem_per_warp(L, R, xm ? 0 : sigma, ring);
+        if (smem > kSmemBudget) continue;
+        const double cost = double(L) * ((xm ? 6.0 : 3.0) * R + 12.0) + 25.0;
+        if (cost < best) {
+          best = cost;
+          out->L = L;
+          out->R = R;
+          out->xm = xm;
+          out->ring = ring;
+          out->smem = smem;
+        }
+      }
+    }
+  }
+  return best < 1e29;
+}
+
+}  // namespace
+
+// ---- context ----------------------------------------------------------------
+struct ap_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex mu;
+  // scratch (grown on demand)
+  uint8_t *d_x = nullptr, *d_y = nullptr, *d_xcode = nullptr, *d_ycode = nullptr, *d_map = nullptr;
+  size_t cap_x = 0, cap_y = 0, cap_xcode = 0, cap_ycode = 0;
+  uint32_t* d_small = nullptr;   // [0] sigma, [1] zero flag
+  uint32_t* h_small = nullptr;   // pinned mirror
+  uint16_t* d_out = nullptr;
+  size_t cap_out = 0;
+  uint4* d_stage = nullptr;
+  size_t cap_stage = 0;
+  unsigned long long* d_cursor = nullptr;
+  unsigned long long* h_cursor = nullptr;  // pinned
+  uint32_t* d_segc = nullptr;
+  size_t cap_segc = 0;
+  unsigned long long* d_offs = nullptr;
+  size_t cap_offs = 0;
+  void* d_cub = nullptr;
+  size_t cap_cub = 0;
+  uint32_t *d_orow = nullptr, *d_ocol = nullptr;
+  uint16_t* d_ohalf = nullptr;
+  size_t cap_orow = 0, cap_ocol = 0, cap_ohalf = 0;
+  float last_ms = 0.f;
+  int last_launches = 0;
+};
+
+namespace {
+
+template <typename T>
+int grow(T** p, size_t* cap, size_t need) {
+  if (*cap >= need && *p) return AP_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  size_t bytes = std::max<size_t>(need, 1) * sizeof(T);
+  CK(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+  *cap = need;
+  return AP_OK;
+}
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+std::mutex g_ctx_mu;
+std::vector<ap_ctx*> g_ctx;
+
+int get_ctx(int device, ap_ctx** out) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ctx.empty()) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      return fail(AP_NODEV, "no CUDA device available (the engine has no CPU fallback)");
+    }
+    g_ctx.assign(n, nullptr);
+  }
+  if (device < 0 || device >= int(g_ctx.size())) return fail(AP_NODEV, "device %d not present", device);
+  if (!g_ctx[device]) {
+    ap_ctx* c = nullptr;
+    int rc = ap_ctx_create(device, &c);
+    if (rc) return rc;
+    g_ctx[device] = c;
+  }
+  *out = g_ctx[device];
+  return AP_OK;
+}
+
+int check_cfg(size_t m, size_t n, const ap_config* cfg) {
+  if (!cfg) return fail(AP_INVALID, "null config");
+  if (cfg->window_w == 0) return fail(AP_CONFIG, "window size must be positive");
+  if (cfg->step_h == 0) return fail(AP_CONFIG, "step size must be positive");
+  if (cfg->blowup_r != 1 && cfg->blowup_r != 2)
+    return fail(AP_CONFIG, "blowup factor must be 1 (LCS) or 2 (alignment score)");
+  if (cfg->window_w > m || cfg->window_w > n)
+    return fail(AP_EMPTY, "no window of size %zu fits inputs of lengths %zu and %zu",
+                size_t(cfg->window_w), m, n);
+  if (cfg->window_w * cfg->blowup_r > AP_MAX_BLOWN_WINDOW)
+    return fail(AP_CONFIG, "CUDA engine supports blown windows up to %d (got %zu)",
+                AP_MAX_BLOWN_WINDOW, size_t(cfg->window_w * cfg->blowup_r));
+  if (n * cfg->blowup_r > 0x7FFFFFF0ull) return fail(AP_CONFIG, "y too long for the CUDA engine");
+  return AP_OK;
+}
+
+// Rows [rb, re) of the grid, clamped.
+int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
+  *rb = cfg->row_begin;
+  *re = cfg->row_end ? std::min<size_t>(cfg->row_end, rows) : rows;
+  if (*rb > *re) return fail(AP_INVALID, "row_begin > row_end");
+  if (*re - *rb > 0xFFFFFFF0ull) return fail(AP_INVALID, "too many rows in one call");
+  return AP_OK;
+}
+
+// Enqueue the whole pipeline for local rows [0, nrows) whose x windows start
+// at d_x (already offset to the first row).  dense: writes d_out.
+int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
+               const ap_config* cfg, size_t nrows, size_t row_global0, bool dense,
+               uint16_t* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
+               uint32_t* d_orow, uint32_t* d_ocol, uint16_t* d_ohalf, size_t cap) {
+  const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
+  const uint32_t W = w * r;
+  const size_t N = n * r;
+  const size_t cols = n - w + 1;
+  c->last_launches = 0;
+  if (nrows == 0) {
+    if (nrec_out) *nrec_out = 0;
+    if (total_out) *total_out = 0;
+    return AP_OK;
+  }
+
+  int rc;
+  // alphabet of y -> dense codes
+  apk::alphabet_kernel<<<1, 1024, 0, st>>>(d_y, n, c->d_map, c->d_small, c->d_small + 1);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->h_small, c->d_small, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const uint32_t sigma_y = c->h_small[0];
+  const uint32_t sent = sigma_y;
+  const uint32_t sigma = sigma_y + (r == 2 ? 1 : 0);
+
+  Shape sh;
+  if (!choose_shape(W, sigma, &sh))
+    return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
+                sigma, W);
+
+  // code streams
+  if ((rc = grow(&c->d_xcode, &c->cap_xcode, mx))) return rc;
+  const size_t ytot = N + 256;
+  if ((rc = grow(&c->d_ycode, &c->cap_ycode, ytot))) return rc;
+  apk::xcode_kernel<<<std::min<size_t>((mx + 255) / 256, 4096), 256, 0, st>>>(d_x, mx, c->d_map,
+                                                                               c->d_xcode);
+  CK(cudaGetLastError());
+  apk::ycode_kernel<<<std::min<size_t>((ytot + 255) / 256, 4096), 256, 0, st>>>(
+      d_y, n, r, sent, c->d_map, c->d_ycode, ytot);
+  CK(cudaGetLastError());
+  c->last_launches += 3;
+
+  KernelFn fn = pick_kernel(sh.L, sh.R, dense, sh.xm);
+  if (!fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", sh.L, sh.R);
+  CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, apk::kWarpsPerCta * 32, sh.smem));
+  if (per_sm < 1) return fail(AP_CONFIG, "kernel L=%d R=%d does not fit an SM", sh.L, sh.R);
+  const size_t total_warps = size_t(c->sms) * per_sm * apk::kWarpsPerCta;
+
+  // column segments: enough independent (strip pair, segment) tasks for ~4
+  // waves, each segment at least 4 windows wide to bound the W-1 overlap.
+  const int G = 32 / sh.L;
+  const size_t npairs = (nrows + 1) / 2;
+  const size_t ngroups = (npairs + G - 1) / G;
+  const size_t out_cols_eff = (N - W) + 1;  // window starts in effective columns (stride 1)
+  size_t nseg = 1;
+  const size_t want = 4 * total_warps;
+  if (ngroups < want) nseg = (want + ngroups - 1) / ngroups;
+  const size_t min_seg = std::max<size_t>(4 * W, 256);
+  nseg = std::min(nseg, std::max<size_t>(1, out_cols_eff / min_seg));
+  size_t S = (out_cols_eff + nseg - 1) / nseg;
+  S = (S + 7) & ~size_t(7);
+  nseg = (out_cols_eff + S - 1) / S;
+
+  apk::CombParams p{};
+  p.xcode = c->d_xcode;
+  p.ycode = c->d_ycode;
+  p.rows = uint32_t(nrows);
+  p.h = h;
+  p.w = w;
+  p.r = r;
+  p.W = W;
+  p.N = uint32_t(N);
+  p.sigma = sh.xm ? 0 : sigma;
+  p.sent_code = sent;
+  p.S = uint32_t(S);
+  p.nseg = uint32_t(nseg);
+  p.ring = sh.ring;
+  p.cols = uint32_t(cols);
+  p.row_global0 = uint32_t(row_global0);
+  p.out = d_out;
+
+  const size_t ntasks = ngroups * nseg;
+  const size_t ctas_needed = (ntasks + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta;
+  const size_t grid = std::min<size_t>(ctas_needed, size_t(c->sms) * per_sm);
+
+  if (!dense) {
+    size_t stage_need = std::max<size_t>(cap, 1 << 16);
+    if (c->cap_stage < stage_need) {
+      int rc2 = grow(&c->d_stage, &c->cap_stage, stage_need);
+      if (rc2) return rc2;
+    }
+    // one extra zero slot so the exclusive scan also yields the total
+    if ((rc = grow(&c->d_segc, &c->cap_segc, nrows * nseg + 1))) return rc;
+    if ((rc = grow(&c->d_offs, &c->cap_offs, nrows * nseg + 1))) return rc;
+    CK(cudaMemsetAsync(c->d_segc + nrows * nseg, 0, sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
+    p.t_half = cfg->threshold_half;
+    p.stage = c->d_stage;
+    p.cursor = c->d_cursor;
+    p.stage_cap = c->cap_stage;
+    p.seg_counts = c->d_segc;
+  }
+
+  CK(cudaEventRecord(c->ev0, st));
+  fn<<<dim3(unsigned(grid)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(p);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev1, st));
+  c->last_launches += 1;
+
+  if (!dense) {
+    // deterministic row-major placement: exclusive scan of (row, segment) counts
+    const size_t nc = nrows * nseg;
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->d_segc, c->d_offs, int(nc + 1), st));
+    if (c->cap_cub < tmp) {
+      if ((rc = grow(reinterpret_cast<unsigned char**>(&c->d_cub), &c->cap_cub, tmp))) return rc;
+    }
+    CK(cub::DeviceScan::ExclusiveSum(c->d_cub, tmp, c->d_segc, c->d_offs, int(nc + 1), st));
+    CK(cudaMemcpyAsync(c->h_cursor, c->d_cursor, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_cursor + 1, c->d_offs + nc, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const size_t nrec = c->h_cursor[0];
+    const size_t total = c->h_cursor[1];
+    if (nrec != total) return fail(AP_CUDA, "threshold bookkeeping mismatch (%zu staged vs %zu counted)", nrec, total);
+    if (nrec > c->cap_stage) {
+      // staging overflowed: grow to the exact size and recompute (rare)
+      if ((rc = grow(&c->d_stage, &c->cap_stage, nrec))) return rc;
+      p.stage = c->d_stage;
+      p.stage_cap = c->cap_stage;
+      CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
+      fn<<<dim3(unsigned(grid)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(p);
+      CK(cudaGetLastError());
+      c->last_launches += 1;
+    }
+    if (nrec && d_orow) {
+      const size_t blocks = std::min<size_t>((nrec + 255) / 256, 8192);
+      apk::place_kernel<<<unsigned(blocks), 256, 0, st>>>(c->d_stage, nrec, c->d_offs,
+                                                            uint32_t(nseg), uint32_t(S), r,
+                                                            uint32_t(row_global0), d_orow, d_ocol,
+                                                            d_ohalf, cap);
+      CK(cudaGetLastError());
+      c->last_launches += 1;
+    }
+    c->last_launches += 2;  // the two cub scan passes
+    *nrec_out = nrec;
+    *total_out = total;
+  }
+  return AP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ap_grid_dims(size_t m, size_t n, size_t w, size_t h, size_t* rows, size_t* cols) {
+  if (!rows || !cols) return fail(AP_INVALID, "null output pointer");
+  if (w == 0 || h == 0) return fail(AP_CONFIG, "window and step must be positive");
+  if (w > m || w > n)
+    return fail(AP_EMPTY, "no window of size %zu fits inputs of lengths %zu and %zu", w, m, n);
+  *rows = (m - w) / h + 1;
+  *cols = n - w + 1;
+  return AP_OK;
+}
+
+int ap_validate(size_t m, size_t n, const ap_config* cfg) { return check_cfg(m, n, cfg); }
+
+const char* ap_last_error(void) { return g_err.c_str(); }
+
+int ap_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int ap_ctx_create(int device, ap_ctx** out) {
+  if (!out) return fail(AP_INVALID, "null ctx pointer");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return fail(AP_NODEV, "no CUDA device available (the engine has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) return fail(AP_NODEV, "device %d not present", device);
+  DevGuard dg(device);
+  ap_ctx* c = new ap_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  c->sms = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+  CK(cudaMalloc(&c->d_small, 64));
+  CK(cudaMallocHost(&c->h_small, 64));
+  CK(cudaMalloc(&c->d_map, 256));
+  CK(cudaMalloc(&c->d_cursor, 16));
+  CK(cudaMallocHost(&c->h_cursor, 32));
+  *out = c;
+  return AP_OK;
+}
+
+int ap_ctx_destroy(ap_ctx* c) {
+  if (!c) return AP_OK;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (auto& p : g_ctx)
+      if (p == c) p = nullptr;
+  }
+  DevGuard dg(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_map,
+                  (void*)c->d_small, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
+                  (void*)c->d_segc, (void*)c->d_offs, c->d_cub, (void*)c->d_orow, (void*)c->d_ocol,
+                  (void*)c->d_ohalf})
+    if (p) cudaFree(p);
+  if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->h_cursor) cudaFreeHost(c->h_cursor);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return AP_OK;
+}
+
+float ap_ctx_last_kernel_ms(ap_ctx* c) {
+  if (!c) return -1.f;
+  DevGuard dg(c->device);
+  float ms = -1.f;
+  if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) != cudaSuccess) {
+    cudaGetLastError();
+    return -1.f;
+  }
+  return ms;
+}
+
+int ap_ctx_last_launches(ap_ctx* c) { return c ? c->last_launches : 0; }
+
+int ap_ctx_plot_dense_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                             const ap_config* cfg, uint16_t* d_out, void* stream) {
+  if (!c || !d_x || !d_y || !d_out) return fail(AP_INVALID, "null argument");
+  int rc = check_cfg(m, n, cfg);
+  if (rc) return rc;
+  size_t rows, cols, rb, re;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
+  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DevGuard dg(c->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const size_t off = rb * cfg->step_h;
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr,
+                    nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y,
+                                 size_t n, const ap_config* cfg, uint64_t* count, uint32_t* d_rows,
+                                 uint32_t* d_cols, uint16_t* d_halves, size_t cap, void* stream) {
+  if (!c || !d_x || !d_y || !count) return fail(AP_INVALID, "null argument");
+  if (cap && (!d_rows || !d_cols || !d_halves)) return fail(AP_INVALID, "null output arrays");
+  int rc = check_cfg(m, n, cfg);
+  if (rc) return rc;
+  size_t rows, cols, rb, re;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
+  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DevGuard dg(c->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const size_t off = rb * cfg->step_h;
+  size_t nrec = 0, total = 0;
+  rc = run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, false, nullptr, st, &nrec, &total,
+                  cap ? d_rows : nullptr, d_cols, d_halves, cap);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(st));
+  *count = total;
+  if (total > cap) return fail(AP_CAPACITY, "%zu cells pass the threshold, capacity %zu", total, cap);
+  return AP_OK;
+}
+
+namespace {
+
+bool has_sentinel(const uint8_t* p, size_t n) { return std::memchr(p, 0, n) != nullptr; }
+
+// Shared host-API body: validates, shards rows over devices, runs, gathers.
+int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+              bool dense, uint16_t* out_half, uint64_t* count, uint32_t* orow, uint32_t* ocol,
+              uint16_t* ohalf, size_t cap) {
+  if (!x || !y || !cfg) return fail(AP_INVALID, "null argument");
+  int rc = check_cfg(m, n, cfg);
+  if (rc) return rc;
+  if (has_sentinel(x, m) || has_sentinel(y, n))
+    return fail(AP_CONFIG, "sequence contains the reserved sentinel code 0");
+  size_t rows, cols, rb, re;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
+  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
+  if (dense && !out_half && re > rb) return fail(AP_INVALID, "null output");
+  const int ndev_avail = ap_device_count();
+  if (ndev_avail <= 0) return fail(AP_NODEV, "no CUDA device available (the engine has no CPU fallback)");
+  int ndev = cfg->n_devices <= 1 ? 1 : std::min(cfg->n_devices, ndev_avail);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  const size_t nr = re - rb;
+  if (size_t(ndev) > nr) ndev = int(std::max<size_t>(nr, 1));
+
+  struct Shard {
+    int dev;
+    size_t r0, r1;
+    size_t total = 0;
+    int rc = AP_OK;
+    std::string err;
+  };
+  std::vector<Shard> sh(ndev);
+  for (int d = 0; d < ndev; ++d) {
+    sh[d].dev = ndev == 1 ? cur : d;
+    sh[d].r0 = rb + nr * d / ndev;
+    sh[d].r1 = rb + nr * (d + 1) / ndev;
+  }
+  const size_t w = cfg->window_w, h = cfg->step_h;
+
+  // phase 1: per device compute (threads so devices overlap)
+  auto work = [&](Shard& s) {
+    ap_ctx* c = nullptr;
+    int e = get_ctx(s.dev, &c);
+    if (e) { s.rc = e; s.err = g_err; return; }
+    std::lock_guard<std::mutex> lk(c->mu);
+    DevGuard dg(c->device);
+    cudaStream_t st = c->stream;
+    const size_t nrows = s.r1 - s.r0;
+    if (nrows == 0) return;
+    const size_t x0 = s.r0 * h, x1 = (s.r1 - 1) * h + w;  // rows plus the w-1 halo
+    auto run = [&]() -> int {
+      int q;
+      if ((q = grow(&c->d_x, &c->cap_x, x1 - x0))) return q;
+      if ((q = grow(&c->d_y, &c->cap_y, n))) return q;
+      CK(cudaMemcpyAsync(c->d_x, x + x0, x1 - x0, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(c->d_y, y, n, cudaMemcpyHostToDevice, st));
+      if (dense) {
+        if ((q = grow(&c->d_out, &c->cap_out, nrows * cols))) return q;
+        if ((q = run_device(c, c->d_x, x1 - x0, c->d_y, n, cfg, nrows, s.r0, true, c->d_out, st,
+                            nullptr, nullptr, nullptr, nullptr, nullptr, 0)))
+          return q;
+        CK(cudaMemcpyAsync(out_half + (s.r0 - rb) * cols, c->d_out, nrows * cols * sizeof(uint16_t),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      } else {
+        // first pass sizes the list (counts are exact even if staging is short)
+        size_t need = std::max<size_t>(cap, 1);
+        if ((q = grow(&c->d_orow, &c->cap_orow, need))) return q;
+        if ((q = grow(&c->d_ocol, &c->cap_ocol, need))) return q;
+        if ((q = grow(&c->d_ohalf, &c->cap_ohalf, need))) return q;
+        size_t nrec = 0, total = 0;
+        if ((q = run_device(c, c->d_x, x1 - x0, c->d_y, n, cfg, nrows, s.r0, false, nullptr, st,
+                            &nrec, &total, c->d_orow, c->d_ocol, c->d_ohalf, need)))
+          return q;
+        CK(cudaStreamSynchronize(st));
+        s.total = total;
+      }
+      return AP_OK;
+    };
+    s.rc = run();
+    if (s.rc) s.err = g_err;
+  };
+  if (ndev == 1) {
+    work(sh[0]);
+  } else {
+    std::vector<std::thread> th;
+    for (auto& s : sh) th.emplace_back(work, std::ref(s));
+    for (auto& t : th) t.join();
+  }
+  for (auto& s : sh)
+    if (s.rc) return fail(s.rc, "%s", s.err.c_str());
+  if (dense) return AP_OK;
+
+  // phase 2: gather per-device counts -> global offsets; copy lists in order
+  uint64_t total = 0;
+  std::vector<uint64_t> offs(ndev);
+  for (int d = 0; d < ndev; ++d) {
+    offs[d] = total;
+    total += sh[d].total;
+  }
+  if (count) *count = total;
+  for (int d = 0; d < ndev; ++d) {
+    if (offs[d] >= cap || sh[d].total == 0) continue;
+    ap_ctx* c = nullptr;
+    get_ctx(sh[d].dev, &c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    DevGuard dg(c->device);
+    const size_t k = std::min<size_t>(sh[d].total, cap - offs[d]);
+    CK(cudaMemcpy(orow + offs[d], c->d_orow, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ocol + offs[d], c->d_ocol, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ohalf + offs[d], c->d_ohalf, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+  }
+  if (total > cap) return fail(AP_CAPACITY, "%llu cells pass the threshold, capacity %zu",
+                               (unsigned long long)total, cap);
+  return AP_OK;
+}
+
+}  // namespace
+
+int ap_plot_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                  uint16_t* out_half) {
+  return host_plot(x, m, y, n, cfg, true, out_half, nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                      uint64_t* count, uint32_t* rows, uint32_t* cols, uint16_t* halves, size_t cap) {
+  if (!count) return fail(AP_INVALID, "null count");
+  if (cap && (!rows || !cols || !halves)) return fail(AP_INVALID, "null output arrays");
+  if (!cfg || !cfg->has_threshold) return fail(AP_INVALID, "ap_plot_threshold needs has_threshold");
+  return host_plot(x, m, y, n, cfg, false, nullptr, count, rows, cols, halves, cap);
+}
+
+}  // extern "C"

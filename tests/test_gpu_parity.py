@@ -1,0 +1,134 @@
+"""GPU parity: the CUDA engine (through the C ABI) vs the oracle and the reference's golden outputs.
+
+Bit-exact comparison (integer work).  Full grids at sizes the oracle finishes
+in seconds; sampled rows (row_begin/row_end) at the BASELINE configs' full
+sizes; thresholded lists compared element by element with apply_threshold.
+"""
+import numpy as np
+import pytest
+
+import golden_util as gu
+import oracle_lib as ol
+from paper_0909_2000_b200 import alignplot as ap
+from paper_0909_2000_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg(w, h, r, t=None, n_devices=1):
+    return ap.PlotConfig(window_w=w, step_h=h, blowup_r=r, threshold_half=t, mode=ap.Mode.cuda,
+                         n_devices=n_devices)
+
+
+def gpu_grid(x, y, w, h, r, row_begin=0, row_end=0):
+    return ap.plot_dense_u16(x, y, cfg(w, h, r), row_begin, row_end).astype(np.int32)
+
+
+@pytest.mark.parametrize("name", ["runner_engines.json", "runner_modes.json"])
+def test_reference_grids(name):
+    for case in gu.load(name)["cases"]:
+        g = gpu_grid(gu.unhex(case["x"]), gu.unhex(case["y"]), case["w"], case["h"], case["r"])
+        assert g.shape == (case["rows"], case["cols"])
+        assert np.array_equal(g.reshape(-1), np.array(case["grid"], dtype=np.int32))
+
+
+def test_reference_acceptance1_540_instances():
+    bad = []
+    for i, case in enumerate(gu.load("acceptance1.json")["cases"]):
+        g = gpu_grid(gu.unhex(case["x"]), gu.unhex(case["y"]), case["w"], case["h"], case["r"])
+        if gu.grid_hash(g) != int(case["hash"]):
+            bad.append((i, case["w"], case["h"], case["r"]))
+    assert not bad, bad[:10]
+
+
+def test_reference_acceptance7():
+    (case,) = gu.load("acceptance7.json")["cases"]
+    g = gpu_grid(gu.unhex(case["x"]), gu.unhex(case["y"]), case["w"], case["h"], case["r"])
+    assert gu.grid_hash(g) == int(case["hash"])
+
+
+def test_compute_plot_matches_oracle_random_shapes():
+    rng = np.random.default_rng(2024)
+    for it in range(60):
+        w = int(rng.integers(1, 130))
+        r = 1 + it % 2
+        m, n = int(rng.integers(w, w + 400)), int(rng.integers(w, w + 700))
+        sigma = [2, 4, 20, 60][it % 4]
+        x = rng.integers(1, sigma + 1, m).astype(np.uint8)
+        y = rng.integers(1, sigma + 1, n).astype(np.uint8)
+        h = int(rng.integers(1, 6))
+        rc, want = ol.plot_rows(x, y, w, h, r)
+        assert rc == 0
+        got = gpu_grid(x, y, w, h, r)
+        assert np.array_equal(got, want), (it, w, h, r, m, n, sigma)
+
+
+def test_config_c1_full_grid():
+    c = datagen.CONFIGS["C1"]
+    x, y = datagen.make_inputs("C1")
+    rc, want = ol.plot_rows(x, y, c.w, c.h, c.r)
+    got = gpu_grid(x, y, c.w, c.h, c.r)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name,rows", [("C2", [0, 1, 2, 3, 4097, 8000, 16284]),
+                                       ("C3", [0, 1, 31337, 65407, 65408]),
+                                       ("C4", [0, 5, 131071, 262080]),
+                                       ("C5", [0, 524287, 1048320])])
+def test_configs_sampled_rows(name, rows):
+    c = datagen.CONFIGS[name]
+    x, y = datagen.make_inputs(name)
+    for rb in rows:
+        re = rb + 2 if name in ("C2", "C3") else rb + 1
+        rc, want = ol.plot_rows(x, y, c.w, c.h, c.r, rb, re)
+        assert rc == 0
+        got = gpu_grid(x, y, c.w, c.h, c.r, rb, re)
+        assert np.array_equal(got, want), (name, rb)
+
+
+def test_threshold_matches_apply_threshold():
+    rng = np.random.default_rng(77)
+    for it in range(20):
+        w = int(rng.integers(4, 80))
+        r = 1 + it % 2
+        m, n = int(rng.integers(w, 600)), int(rng.integers(w, 900))
+        x = rng.integers(1, 5, m).astype(np.uint8)
+        y = x[rng.integers(0, m, n)] if it % 3 == 0 else rng.integers(1, 5, n).astype(np.uint8)
+        h = 1 + it % 3
+        rc, grid = ol.plot_rows(x, y, w, h, r)
+        t = int(np.quantile(grid, 0.97))
+        rr, cc = np.nonzero(grid >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc)
+        assert np.array_equal(gh, grid[rr, cc])
+
+
+def test_threshold_planted_homology():
+    # x and y share long blocks, so thresholded hits are dense along diagonals
+    rng = np.random.default_rng(5)
+    x = rng.integers(1, 5, 3000).astype(np.uint8)
+    y = np.concatenate([rng.integers(1, 5, 400), x[500:1500], rng.integers(1, 5, 300), x[2000:2600]]).astype(np.uint8)
+    w, h, r = 64, 1, 1
+    rc, grid = ol.plot_rows(x, y, w, h, r)
+    t = 2 * 60
+    rr, cc = np.nonzero(grid >= t)
+    assert rr.size > 1000
+    gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
+    assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, grid[rr, cc])
+
+
+def test_errors_before_device_work():
+    with pytest.raises(ap.EmptyPlotError):
+        ap.compute_plot(ap.Sequence("x", [1, 2, 1]), ap.Sequence("y", [2, 1, 2]), cfg(10, 1, 1))
+    with pytest.raises(ap.ConfigError):
+        ap.compute_plot(ap.Sequence("x", [1, 2, 1]), ap.Sequence("y", [2, 1, 2]), cfg(2, 1, 7))
+    with pytest.raises(ap.ConfigError):
+        ap.plot_dense_u16(np.array([1, 0, 2], np.uint8), np.array([1, 2, 2], np.uint8), cfg(2, 1, 1))
+
+
+def test_window_equals_input():
+    x = np.array([1, 2, 3, 1, 2], np.uint8)
+    g = gpu_grid(x, x, 5, 1, 1)
+    assert g.shape == (1, 1) and g[0, 0] == 10
+    g = gpu_grid(x, x, 5, 1, 2)
+    assert g[0, 0] == 10
