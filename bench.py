@@ -1,0 +1,417 @@
+#!/usr/bin/env python3
+"""Benchmark of the alignment-plot hot path (BASELINE.json metric: window-pair cell updates/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl engine|reference]
+
+A *step* is one pass of the hot path over one full plot of the workload: the
+code-stream kernels plus the fused comb+extract kernel writing the dense
+uint16 grid (C1/C2) or the thresholded row-major list (C3-C5).  The default
+workload is BASELINE.json configs[1] = C2 (alignment-score plot, m=16384,
+w=100, dense), which fits one B200.
+
+* ``value``  — WPCU/s = rows*cols*w / t over all ranks, inputs resident in HBM
+  (ap_ctx_*_device), timed with CUDA events on the launching stream, L2
+  flushed (256 MiB write) between steps outside the timed events.
+* ``e2e``    — the same metric through the public host API (ap_plot_dense /
+  ap_plot_threshold) with pinned host buffers: H2D of x,y and D2H of the plot
+  inside the timed region.
+* ``roofline`` — the comb kernel against the measured integer-ALU issue peak
+  (profiles/int_peak_r01.json x the SM clock sampled during the run); the
+  algorithmic work is 3 int32 lane-ops per comb cell (SURVEY.md §8d basis),
+  comb cells = rows * (w*r) * (n*r).
+* ``cpu_baseline`` — the unmodified reference library (oracle/_ref, sea8 /
+  sea16, all host cores) on a bounded row sample of the same workload.
+
+Multi-GPU (torchrun): rows of an N-times-taller x (the workload's x followed by
+seeded uniform DNA) shard over ranks with a w-1 halo; per-rank work is fixed
+(weak scaling); the time is the max over ranks; thresholded configs all_gather
+one hit count per rank (NCCL), dense ones exchange nothing.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_0909_2000_b200 import datagen  # noqa: E402
+from paper_0909_2000_b200.sharding import plan_row_shards, shard_x  # noqa: E402
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+INT_PEAK = os.path.join(ROOT, "profiles", "int_peak_r01.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---- clocks -------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- workload -------------------------------------------------------------------------------
+def workload(name: str, world: int):
+    c = datagen.CONFIGS[name]
+    x, y = datagen.make_inputs(name)
+    if world > 1:
+        # weak scaling: x grows by world; each rank gets the base workload's row count
+        extra = datagen.uniform(1000 + world, 7, (world - 1) * x.size, datagen.DNA if name != "C4" else datagen.PROTEIN)
+        x = np.concatenate([x, extra])
+    return c, x, y
+
+
+def comb_cells(rows, c, n):
+    return rows * (c.w * c.r) * (n * c.r)
+
+
+# ---- reference CPU arm ------------------------------------------------------------------------
+def reference_rows_rate(c, x, y, budget_s: float, max_rows: int):
+    """Time the unmodified reference (oracle/_ref) on a bounded, evenly spaced row sample.
+
+    Returns (rows_done, seconds, cores, sample_desc)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as ol
+
+    if not ol.ref_available():
+        return None
+    cores = os.cpu_count() or 1
+    mode = ol.SEA8 if c.w <= 254 else ol.SEA16
+    rows_total = (x.size - c.w) // c.h + 1
+    # calibrate on a small block
+    blk = max(cores, 8)
+    t0 = time.perf_counter()
+    rc, g, err = ol.ref_plot_rows(x, y, c.w, c.h, c.r, 0, min(blk, rows_total), mode, cores)
+    t_cal = time.perf_counter() - t0
+    if rc:
+        raise RuntimeError(f"reference failed: {err}")
+    per_row = t_cal / min(blk, rows_total)
+    nrows = int(min(max_rows, rows_total, max(blk, budget_s / max(per_row, 1e-9))))
+    nblocks = max(1, nrows // blk)
+    starts = np.linspace(0, rows_total - blk, nblocks).astype(int) if rows_total > blk else [0]
+    done = 0
+    t0 = time.perf_counter()
+    for s in starts:
+        e = min(rows_total, int(s) + blk)
+        rc, g, err = ol.ref_plot_rows(x, y, c.w, c.h, c.r, int(s), e, mode, cores)
+        if rc:
+            raise RuntimeError(f"reference failed: {err}")
+        done += e - int(s)
+    dt = time.perf_counter() - t0
+    desc = (f"{done} of {rows_total} grid rows ({len(starts)} evenly spaced blocks of {blk}), "
+            f"reference compute_plot mode={'sea8' if mode == ol.SEA8 else 'sea16'}, workers={cores}")
+    return done, dt, cores, desc
+
+
+def run_reference(args, rank, world):
+    c, x, y = workload(args.config, 1)
+    rows_total, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
+    metric_unit = "window-pair cell updates/s"
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as ol
+    if not ol.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libalignplot_ref.so not built"}))
+        return
+    vals = []
+    t_all = 0.0
+    rows_all = 0
+    for _ in range(args.steps):
+        done, dt, cores, desc = reference_rows_rate(c, x, y, budget_s=args.ref_seconds / max(1, args.steps),
+                                                    max_rows=rows_total)
+        vals.append(done * cols * c.w / dt)
+        t_all += dt
+        rows_all += done
+    value = rows_all * cols * c.w / t_all
+    line = {
+        "metric": "window-pair cell updates/s (m*n*w/s)", "value": value, "unit": metric_unit,
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * t_all / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (paper_0909_2000_b200.datagen)",
+        "config": config_desc(c, x, y, 1, args.config),
+        "cpu_baseline": {"value": value, "unit": metric_unit, "cores": cores, "kind": "reference",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": metric_unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_desc(c, x, y, world, name):
+    rows, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
+    return {"workload": f"{name}: {c.description}", "m": int(x.size), "n": int(y.size), "w": c.w, "h": c.h,
+            "r": c.r, "rows": rows, "cols": cols,
+            "output": "dense uint16 half-units" if c.t_half is None else f"threshold half >= {c.t_half}, row-major list",
+            "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+            "l2": "flushed between steps (256 MiB write, outside the timed events)"}
+
+
+# ---- engine arm -------------------------------------------------------------------------------
+def run_engine(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_0909_2000_b200 import _native
+    from paper_0909_2000_b200 import alignplot as ap
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c, x, y = workload(args.config, world)
+    shard = plan_row_shards(x.size, c.w, c.h, world)[rank]
+    xs = shard_x(x, shard)
+    n = y.size
+    rows_local, cols = shard.rows, n - c.w + 1
+    rows_global = (x.size - c.w) // c.h + 1
+    L = _native.lib()
+    ctx = ctypes.c_void_p()
+    rc = L.ap_ctx_create(local_rank, ctypes.byref(ctx))
+    if rc:
+        raise RuntimeError(_native.last_error())
+    cfgc = _native.ApConfig(window_w=c.w, step_h=c.h, blowup_r=c.r, has_threshold=0 if c.t_half is None else 1,
+                            threshold_half=c.t_half or 0, n_devices=1, row_begin=0, row_end=0)
+    d_x = torch.from_numpy(xs.copy()).to(dev)
+    d_y = torch.from_numpy(y.copy()).to(dev)
+    dense = c.t_half is None
+    cap = 0
+    if dense:
+        d_out = torch.empty(rows_local * cols, dtype=torch.int16, device=dev)
+    else:
+        cap = 1 << 22
+        d_r = torch.empty(cap, dtype=torch.int32, device=dev)
+        d_c = torch.empty(cap, dtype=torch.int32, device=dev)
+        d_h = torch.empty(cap, dtype=torch.int16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    count = ctypes.c_uint64(0)
+
+    def step():
+        if dense:
+            rc = L.ap_ctx_plot_dense_device(ctx, d_x.data_ptr(), xs.size, d_y.data_ptr(), n, ctypes.byref(cfgc),
+                                            d_out.data_ptr(), stream.cuda_stream)
+        else:
+            rc = L.ap_ctx_plot_threshold_device(ctx, d_x.data_ptr(), xs.size, d_y.data_ptr(), n,
+                                                ctypes.byref(cfgc), ctypes.byref(count), d_r.data_ptr(),
+                                                d_c.data_ptr(), d_h.data_ptr(), cap, stream.cuda_stream)
+        if rc not in (0, _native.AP_CAPACITY):
+            raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ms, launches = [], 0
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+            kern_ms.append(L.ap_ctx_last_kernel_ms(ctx))
+            launches += L.ap_ctx_last_launches(ctx)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_local = sum(step_ms) / 1000.0
+    kern_local = sum(kern_ms) / len(kern_ms) / 1000.0
+    t = torch.tensor([t_local, kern_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max, kern_max = float(t[0]), float(t[1])
+    hits_local = int(count.value) if not dense else 0
+
+    # ---- end to end through the public host API (pinned host buffers) ----
+    hx = torch.from_numpy(xs.copy()).pin_memory()
+    hy = torch.from_numpy(y.copy()).pin_memory()
+    cfg_py = ap.PlotConfig(window_w=c.w, step_h=c.h, blowup_r=c.r, threshold_half=c.t_half, mode=ap.Mode.cuda)
+    if dense:
+        hout = torch.empty(rows_local * cols, dtype=torch.int16).pin_memory()
+    else:
+        cap_h = max(1, hits_local)
+        hr = torch.empty(cap_h, dtype=torch.int32).pin_memory()
+        hc = torch.empty(cap_h, dtype=torch.int32).pin_memory()
+        hh = torch.empty(cap_h, dtype=torch.int16).pin_memory()
+    apc = ap._cfg(cfg_py)
+
+    def e2e_step():
+        if dense:
+            rc = L.ap_plot_dense(hx.data_ptr(), xs.size, hy.data_ptr(), n, ctypes.byref(apc), hout.data_ptr())
+        else:
+            rc = L.ap_plot_threshold(hx.data_ptr(), xs.size, hy.data_ptr(), n, ctypes.byref(apc), ctypes.byref(count),
+                                     hr.data_ptr(), hc.data_ptr(), hh.data_ptr(), cap_h)
+        if rc:
+            raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
+
+    torch.cuda.set_device(local_rank)
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    t_e2e_local = time.perf_counter() - t0
+    te = torch.tensor([t_e2e_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te[0])
+    d2h = rows_local * cols * 2 if dense else hits_local * 10 + 8
+
+    if rank != 0:
+        L.ap_ctx_destroy(ctx)
+        return
+    wpcu = rows_global * cols * c.w
+    value = wpcu * args.steps / t_max
+    clocks = clk.summary()
+    cells_local = comb_cells(rows_local, c, n)
+    peak_ops_clk = None
+    if os.path.exists(INT_PEAK):
+        with open(INT_PEAK) as f:
+            peak_ops_clk = json.load(f).get("lane_ops_per_clk_per_sm")
+    sm_mhz = clocks["sm_mhz"] or 1965.0
+    props = torch.cuda.get_device_properties(dev)
+    roof = None
+    if peak_ops_clk:
+        peak = props.multi_processor_count * peak_ops_clk * sm_mhz * 1e6 / 1e12
+        achieved = cells_local * 3 / kern_max / 1e12
+        roof = {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
+                "frac": achieved / peak, "traffic": None,
+                "basis": "3 int32 lane-ops per comb cell (SURVEY §8d), cells = rows*(w*r)*(n*r); peak = "
+                         f"{props.multi_processor_count} SMs x {peak_ops_clk:.1f} measured lane-ops/clk/SM x "
+                         f"{sm_mhz:.0f} MHz (median SM clock during the run)",
+                "kernel_ms": kern_max * 1000.0, "comb_cells_per_s": cells_local / kern_max}
+    hbm = None
+    if os.path.exists(MEASURED_PEAKS):
+        with open(MEASURED_PEAKS) as f:
+            hbm_peak = json.load(f).get("hbm_gbs")
+        out_bytes = rows_local * cols * 2 if dense else hits_local * 10 + 8
+        hbm = {"bound": "hbm", "achieved": out_bytes / kern_max / 1e9, "peak": hbm_peak, "unit": "GB/s",
+               "frac": out_bytes / kern_max / 1e9 / hbm_peak if hbm_peak else None,
+               "what": "plot output stream written by the comb kernel"}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        res = reference_rows_rate(c, x, y, budget_s=args.ref_seconds, max_rows=rows_global)
+        if res:
+            done, dt, cores, desc = res
+            cpu = {"value": done * cols * c.w / dt, "unit": "window-pair cell updates/s", "cores": cores,
+                   "kind": "reference", "sample": desc}
+    line = {
+        "metric": "window-pair cell updates/s (m*n*w/s)", "value": value, "unit": "window-pair cell updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+        "data": "synthetic (seeded, paper_0909_2000_b200.datagen)",
+        "config": config_desc(c, x, y, world, args.config),
+        "entries_per_s": rows_global * cols * args.steps / t_max,
+        "comb_cells_per_s": comb_cells(rows_global, c, n) * args.steps / t_max,
+        "roofline": roof, "roofline_hbm_output": hbm, "clocks": clocks,
+        "e2e": {"value": wpcu * args.steps / t_e2e, "unit": "window-pair cell updates/s",
+                "h2d_bytes_per_step": int(xs.size + n), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches, "cpu_baseline": cpu,
+    }
+    if not dense:
+        line["hits_rank0"] = hits_local
+    print(json.dumps(line), flush=True)
+    L.ap_ctx_destroy(ctx)
+
+
+def main():
+    ap_ = argparse.ArgumentParser()
+    ap_.add_argument("--gpus", type=int, default=1)
+    ap_.add_argument("--steps", type=int, default=10)
+    ap_.add_argument("--warmup", type=int, default=3)
+    ap_.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS))
+    ap_.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap_.add_argument("--ref-seconds", type=float, default=8.0, help="wall-clock budget of the CPU reference sample")
+    ap_.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap_.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "engine":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_engine(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,43 +48,27 @@ int fail(int code, const char* fmt, ...) {
 
 // ---- kernel shape table ---------------------------------------------------
 using KernelFn = void (*)(apk::CombParams);
+constexpr int kBands = 2;
 
 template <int L, int R, bool XM>
 KernelFn pick_fn(bool dense) {
-  return dense ? reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, true, XM>)
-               : reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, false, XM>);
+  return dense ? reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, kBands, true, XM>)
+               : reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, kBands, false, XM>);
 }
-
-// Table kernels: R in {4, 8, ..., 32}; computed-mask kernels: R in {8, 16, 32}.
-constexpr int kXmRs[] = {8, 16, 32};
 
 template <int L>
 KernelFn pick_r(int R, bool dense, bool xm) {
-  if (xm) {
-    switch (R) {
-      case 8: return pick_fn<L, 8, true>(dense);
-      case 16: return pick_fn<L, 16, true>(dense);
-      case 32: return pick_fn<L, 32, true>(dense);
-    }
-    return nullptr;
-  }
   switch (R) {
-    case 4: return pick_fn<L, 4, false>(dense);
-    case 8: return pick_fn<L, 8, false>(dense);
-    case 12: return pick_fn<L, 12, false>(dense);
-    case 16: return pick_fn<L, 16, false>(dense);
-    case 20: return pick_fn<L, 20, false>(dense);
-    case 24: return pick_fn<L, 24, false>(dense);
-    case 28: return pick_fn<L, 28, false>(dense);
-    case 32: return pick_fn<L, 32, false>(dense);
+    case 8: return xm ? pick_fn<L, 8, true>(dense) : pick_fn<L, 8, false>(dense);
+    case 16: return xm ? pick_fn<L, 16, true>(dense) : pick_fn<L, 16, false>(dense);
+    case 24: return xm ? pick_fn<L, 24, true>(dense) : pick_fn<L, 24, false>(dense);
+    case 32: return xm ? pick_fn<L, 32, true>(dense) : pick_fn<L, 32, false>(dense);
   }
   return nullptr;
 }
 
 KernelFn pick_kernel(int L, int R, bool dense, bool xm) {
   switch (L) {
-    case 2: return pick_r<2>(R, dense, xm);
-    case 4: return pick_r<4>(R, dense, xm);
     case 8: return pick_r<8>(R, dense, xm);
     case 16: return pick_r<16>(R, dense, xm);
     case 32: return pick_r<32>(R, dense, xm);
@@ -92,7 +76,7 @@ KernelFn pick_kernel(int L, int R, bool dense, bool xm) {
   return nullptr;
 }
 
-constexpr size_t kSmemBudget = 200 * 1024;  // per CTA (4 warps)
+constexpr size_t kSmemPerSm = 227 * 1024;
 
 uint32_t next_pow2(uint32_t v) {
   uint32_t p = 1;
@@ -105,24 +89,35 @@ struct Shape {
   bool xm = false;   // masks computed in registers (no table)
   uint32_t ring = 0;
   size_t smem = 0;
+  int warps_per_sm = 0;
 };
 
-// Cost model per strip pair and column: L lanes x (3 ops per row pair + ~12
-// per-step overhead) + ~25 extraction ops per column.  Feasible shapes must
-// cover W rows and fit the per-warp mismatch table in shared memory.
-bool choose_shape(uint32_t W, uint32_t sigma, Shape* out) {
+// Cost per strip pair and column: L lanes x (3 ops per row pair [6 with computed
+// masks] + ~14 per-step overhead) + ~25 extraction ops, scaled up when fewer than
+// 16 warps per SM fit (registers from the compiled kernel, table in shared memory).
+bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
   const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
   double best = 1e30;
   for (int xm = 0; xm < 2; ++xm) {
-    for (int L : {2, 4, 8, 16, 32}) {
-      for (int R = 4; R <= 32; R += 4) {
-        if (xm && R != 8 && R != 16 && R != 32) continue;
+    for (int L : {8, 16, 32}) {
+      for (int R : {8, 16, 24, 32}) {
         if (uint32_t(L * R) < W) continue;
-        if (!xm && uint32_t(L * (R - 4)) >= W && R > 4) continue;  // smaller R covers W
-        const size_t smem =
-            apk::kWarpsPerCta * apk::comb_smem_per_warp(L, R, xm ? 0 : sigma, ring);
-        if (smem > kSmemBudget) continue;
-        const double cost = double(L) * ((xm ? 6.0 : 3.0) * R + 12.0) + 25.0;
+        KernelFn fn = pick_kernel(L, R, dense, xm);
+        if (!fn) continue;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+        const size_t smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(L, R, xm ? 0 : sigma, ring);
+        if (smem > kSmemPerSm - 1024) continue;
+        const int by_regs = 65536 / (std::max(fa.numRegs, 1) * 32 * apk::kWarpsPerCta);
+        const int by_smem = int(kSmemPerSm / (smem + 1024));
+        const int ctas = std::min({by_regs, by_smem, 16});
+        if (ctas < 1) continue;
+        const int warps = ctas * apk::kWarpsPerCta;
+        double cost = double(L) * ((xm ? 6.0 : 3.0) * R + 14.0) + 25.0;
+        if (warps < 16) cost *= 16.0 / warps;
         if (cost < best) {
           best = cost;
           out->L = L;
@@ -130,6 +125,7 @@ bool choose_shape(uint32_t W, uint32_t sigma, Shape* out) {
           out->xm = xm;
           out->ring = ring;
           out->smem = smem;
+          out->warps_per_sm = warps;
         }
       }
     }
@@ -272,7 +268,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const uint32_t sigma = sigma_y + (r == 2 ? 1 : 0);
 
   Shape sh;
-  if (!choose_shape(W, sigma, &sh))
+  if (!choose_shape(W, sigma, dense, &sh))
     return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                 sigma, W);
 
@@ -309,7 +305,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t min_seg = std::max<size_t>(4 * W, 256);
   nseg = std::min(nseg, std::max<size_t>(1, out_cols_eff / min_seg));
   size_t S = (out_cols_eff + nseg - 1) / nseg;
-  S = (S + 7) & ~size_t(7);
+  S = (S + 31) & ~size_t(31);   // segment starts 32-aligned: 16-B vector loads of the code stream
   nseg = (out_cols_eff + S - 1) / S;
 
   apk::CombParams p{};

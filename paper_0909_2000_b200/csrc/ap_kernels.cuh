@@ -47,8 +47,8 @@ namespace apk {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kChunk = 32;          // steps per extraction batch
-constexpr uint32_t kRebaseAt = 0xF000u;
-constexpr uint32_t kRebaseBy = 0x8000u;
+constexpr uint32_t kRebaseAt = 0x7000u;   // fresh keys must stay fp16-finite (<= 0x7BFF)
+constexpr uint32_t kRebaseBy = 0x4000u;
 
 struct CombParams {
   const uint8_t* xcode;   // mapped x codes (0xFF = absent from y), local row 0 at xcode[0]
@@ -57,7 +57,7 @@ struct CombParams {
   uint32_t h, w, r, W, N; // step, window, blowup, blown window, effective y length
   uint32_t sigma;         // table codes (incl. the sentinel code when r = 2)
   uint32_t sent_code;     // code of the $ sentinel (r = 2)
-  uint32_t S;             // column segment width (effective columns), multiple of 8
+  uint32_t S;             // column segment width (effective columns), multiple of 32
   uint32_t nseg;          // number of column segments
   uint32_t ring;          // ok-flag ring size (power of two >= W + 64)
   uint32_t cols;          // grid columns
@@ -70,9 +70,16 @@ struct CombParams {
   unsigned long long* cursor;     // staging append cursor
   unsigned long long stage_cap;
   uint32_t* seg_counts;           // [rows][nseg] hits per (row, segment)
+  uint32_t zero;                  // always 0 (HFMA2 addend)
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ uint32_t lop3_xor(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 
 // PRMT with sign replication (selector nibble bit 3); __byte_perm masks it off.
 __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t sel) {
@@ -84,34 +91,58 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t sel) {
 // Shared memory bytes per warp for a (L, R) instantiation.
 __host__ __device__ inline size_t comb_smem_per_warp(int L, int R, uint32_t sigma, uint32_t ring) {
   const int G = 32 / L;
-  return size_t(128) * sigma * R          // mismatch table (sigma = 0 when masks are computed)
-       + size_t(G) * kChunk * 4           // bottom-key ring per group
-       + size_t(G) * 2 * ring;            // ok flags per group (strip A, strip B)
+  const size_t bytes = size_t(128) * sigma * R   // mismatch table (sigma = 0 when masks are computed)
+       + size_t(G) * (kChunk + 1) * 4            // bottom-key ring per group (padded: no bank conflicts)
+       + size_t(G) * 2 * ring;                   // ok flags per group (strip A, strip B)
+  return (bytes + 15) & ~size_t(15);             // keep every warp's table 16-B aligned
 }
 
-// XM = false: mismatch masks from the shared-memory table (small alphabets).
-// XM = true : masks computed in registers from the x-code pairs (any alphabet):
-//   e = (xpair ^ y*0x10001) + 0x7FFF7FFF has bit 15 of a half set iff the codes
-//   differ; PRMT's sign-replicate mode (selector 0xBB99) widens it to 0xFFFF.
-template <int L, int R, bool DENSE, bool XM>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+// Comb kernel (K2): fused $-interleave, seaweed combing, window extraction
+// and output for one (strip-pair group, column segment) task per warp.
+//
+// Shape: L lanes per strip pair, R rows per lane, split into K bands of R/K
+// rows.  Band b of lane j ("virtual band" v = j*K + b) processes column s - v
+// at step s, so the K chains of a lane are independent within a step (ILP K);
+// band 0 gets the seaweed leaving lane j-1's last band one step earlier via
+// SHFL, band b>0 the one its own band b-1 produced one step earlier.  The y
+// codes travel the same way, one step ahead, so the mismatch-table rows of
+// step s+1 are loaded from shared memory during step s.
+//
+// XM = false (small alphabets): per-warp table M[code][row] holding, per
+//   16-bit half, the fp16 multiplier 1.0 (0x3C00, mismatch) or 0 (match);
+//   t = T * M runs as HFMA2 on the FMA pipe, so a cell pair costs
+//   HFMA2 + VIMNMX.U16x2 + LOP3 (two ALU-pipe ops).  Keys stay in [0, 0x7BFF]
+//   (positive finite fp16 patterns: x*1 = x, x*0 = +0, verified on B200 by
+//   tools/int_peak.cu).
+// XM = true (any alphabet): NF computed from the x-code pair registers:
+//   e = (xpair ^ y*0x10001) + 0x7FFF7FFF has bit 15 of a half set iff the
+//   codes differ; PRMT's sign-replicate mode (selector 0xBB99) widens it to
+//   0xFFFF; t = T & NF.
+template <int L, int R, int K, bool DENSE, bool XM>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
-  static_assert(32 % L == 0 && R % 4 == 0, "bad shape");
+  static_assert(32 % L == 0 && L >= 8, "table layout needs L >= 8 (conflict-free LDS.128)");
+  static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
   constexpr int G = 32 / L;
-  constexpr int Q = R / 4;
+  constexpr int Q = R / 4;        // quads per lane
+  constexpr int RB = R / K;       // rows per band
+  constexpr int QB = RB / 4;      // quads per band
+  constexpr int VB = L * K;       // virtual bands per strip (wavefront depth)
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
   const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t g = lane / L;     // group within warp
-  const uint32_t j = lane % L;     // lane within group
+  const uint32_t g = lane / L;
+  const uint32_t j = lane % L;
   const size_t per_warp = comb_smem_per_warp(L, R, p.sigma, p.ring);
   unsigned char* wbase = smem + warp * per_warp;
   uint4* tbl = reinterpret_cast<uint4*>(wbase);                       // [G][sigma][Q][L]
-  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + size_t(128) * p.sigma * R) + g * kChunk;
-  uint8_t* okA = wbase + size_t(128) * p.sigma * R + G * kChunk * 4 + size_t(g) * 2 * p.ring;
+  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + size_t(128) * p.sigma * R) + g * (kChunk + 1);
+  uint8_t* okA = wbase + size_t(128) * p.sigma * R + G * (kChunk + 1) * 4 + size_t(g) * 2 * p.ring;
   uint8_t* okB = okA + p.ring;
   const uint32_t rmask = p.ring - 1;
+  const uint32_t rshift = p.r - 1;
+  const uint32_t zero = p.zero;   // 0, opaque to ptxas so the HFMA2 is not folded into HMUL2
 
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + G - 1) / G;
@@ -124,12 +155,12 @@ comb_kernel(const CombParams p) {
     const uint32_t pair = pg * G + g;
     const uint32_t rA = 2 * pair, rB = 2 * pair + 1;
     const bool hasA = rA < p.rows, hasB = rB < p.rows;
-    const uint32_t c0 = seg * p.S;                       // first effective column of the segment
+    const uint32_t c0 = seg * p.S;
     const uint32_t nseg_cols = min(p.S + p.W - 1, p.N - c0);
-    const uint32_t nsteps = nseg_cols + L - 1;
+    const uint32_t nsteps = nseg_cols + VB - 1;
     const uint32_t nch = (nsteps + kChunk - 1) / kChunk;
 
-    // ---- mismatch table for this strip pair (fused $-interleave, scoring.cpp:5-17)
+    // ---- mismatch table / x-code registers (fused $-interleave, scoring.cpp:5-17)
     __syncwarp();
     uint32_t xpair[XM ? R : 1];
     {
@@ -137,13 +168,13 @@ comb_kernel(const CombParams p) {
 #pragma unroll
       for (int rho = 0; rho < R; ++rho) {
         const uint32_t i = j * R + rho;
-        uint32_t ca = 0x1FFu, cb = 0x1FFu;  // 0x1FF: never equals a code
+        uint32_t ca = 0x1FFu, cb = 0x1FFu;  // never equals a code (pad rows, missing strips)
         if (i < p.W) {
           if (p.r == 2 && !(i & 1u)) {
             ca = hasA ? p.sent_code : 0x1FFu;
             cb = hasB ? p.sent_code : 0x1FFu;
           } else {
-            const uint32_t xi = (p.r == 2) ? (i >> 1) : i;
+            const uint32_t xi = i >> rshift;
             if (hasA) ca = p.xcode[size_t(rA) * p.h + xi];
             if (hasB) cb = p.xcode[size_t(rB) * p.h + xi];
             if (ca == 0xFFu) ca = 0x1FFu;   // byte absent from y: never matches
@@ -156,18 +187,19 @@ comb_kernel(const CombParams p) {
       if constexpr (XM) {
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) xpair[rho] = xa[rho] | (xb[rho] << 16);
-      }
-      uint4* tg = tbl + size_t(g) * p.sigma * Q * L;
-      for (uint32_t a = 0; a < (XM ? 0u : p.sigma); ++a) {
+      } else {
+        uint4* tg = tbl + size_t(g) * p.sigma * Q * L;
+        for (uint32_t a = 0; a < p.sigma; ++a) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          uint32_t wv[4];
+          for (int q = 0; q < Q; ++q) {
+            uint32_t wv[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int rho = 4 * q + k;
-            wv[k] = (xa[rho] == a ? 0u : 0x0000FFFFu) | (xb[rho] == a ? 0u : 0xFFFF0000u);
+            for (int k = 0; k < 4; ++k) {
+              const int rho = 4 * q + k;
+              wv[k] = (xa[rho] == a ? 0u : 0x00003C00u) | (xb[rho] == a ? 0u : 0x3C000000u);
+            }
+            tg[(a * Q + q) * L + j] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
           }
-          tg[(a * Q + q) * L + j] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
       for (uint32_t k = j; k < 2 * p.ring; k += L) okA[k] = 0;
@@ -179,70 +211,118 @@ comb_kernel(const CombParams p) {
 
     uint32_t V[R];
 #pragma unroll
-    for (int rho = 0; rho < R; ++rho) V[rho] = 0u;   // left-boundary seaweeds: key 0
-    uint32_t tout = 0u;                              // virtual columns carry key 0 (harmless)
-    uint32_t yprev = 0u;
-    int32_t kbase = -int32_t(p.W) - 1;               // key(c) = c - kbase > W for every top seaweed
-    uint32_t fresh = uint32_t(-kbase) * 0x00010001u;
-    uint32_t run = 0u;                               // packed window counts (A | B << 16)
+    for (int rho = 0; rho < R; ++rho) V[rho] = 0u;     // left-boundary seaweeds: key 0
+    uint32_t tb[K];     // seaweed leaving band b at the previous step
+    uint32_t cd[K];     // y code of band b at the current step
+#pragma unroll
+    for (int b = 0; b < K; ++b) { tb[b] = 0u; cd[b] = 0u; }
+    int32_t kbase = -int32_t(p.W) - 1;                 // key(c) = c - kbase > W for top seaweeds
+    uint32_t fresh = uint32_t(-kbase) * 0x00010001u;   // key of column s, both halves
+    uint32_t run = 0u;
     uint32_t hitsA = 0u, hitsB = 0u;
 
-    uint64_t ycur = __ldg(yw);
+    // lane 0's y codes: one 32-byte chunk of the code stream per 32 steps, prefetched
+    uint4 ych = __ldg(reinterpret_cast<const uint4*>(yw));
+    uint4 ych2 = __ldg(reinterpret_cast<const uint4*>(yw) + 1);
+    if (j == 0) cd[0] = ych.x & 0xFFu;                 // column 0
+
     for (uint32_t ch = 0; ch < nch; ++ch) {
-#pragma unroll 1
-      for (int sub = 0; sub < kChunk / 8; ++sub) {
-        const uint32_t s0 = ch * kChunk + sub * 8;
-        const uint64_t ynext = __ldg(yw + (s0 >> 3) + 1);
+      const uint32_t yc_words[8] = {ych.x, ych.y, ych.z, ych.w, ych2.x, ych2.y, ych2.z, ych2.w};
+      const uint4 nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
+      const uint4 nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t y0 = uint32_t(ycur >> (8 * u)) & 0xFFu;
-          uint32_t yc = __shfl_up_sync(0xFFFFFFFFu, yprev, 1, L);
-          uint32_t tin = __shfl_up_sync(0xFFFFFFFFu, tout, 1, L);
-          if (j == 0) { yc = y0; tin = fresh; }
-          fresh += 0x00010001u;
-          const uint4* tp = tl + yc * (Q * L);
-          const uint32_t yrep = yc * 0x00010001u;
+      for (int u = 0; u < kChunk; ++u) {
+        // table quads of this step (codes known since the previous step)
+        uint4 nfq[Q];
+        if constexpr (!XM) {
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            uint32_t nfv[4];
+          for (int b = 0; b < K; ++b)
+#pragma unroll
+            for (int qq = 0; qq < QB; ++qq) nfq[b * QB + qq] = tl[(cd[b] * Q + b * QB + qq) * L];
+        }
+        // seaweeds entering each band
+        uint32_t tin[K];
+        {
+          const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, tb[K - 1], 1, L);
+          tin[0] = j == 0 ? fresh : sh;
+#pragma unroll
+          for (int b = 1; b < K; ++b) tin[b] = tb[b - 1];
+        }
+        fresh += 0x00010001u;
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          uint32_t t = tin[b];
+          const uint32_t yrep = cd[b] * 0x00010001u;
+#pragma unroll
+          for (int qq = 0; qq < QB; ++qq) {
+            uint32_t m[4];
             if constexpr (XM) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                nfv[k] = prmt_sign((xpair[4 * q + k] ^ yrep) + 0x7FFF7FFFu, 0xBB99u);
+                m[k] = prmt_sign((xpair[b * RB + 4 * qq + k] ^ yrep) + 0x7FFF7FFFu, 0xBB99u);
             } else {
-              const uint4 nf = tp[q * L];
-              nfv[0] = nf.x; nfv[1] = nf.y; nfv[2] = nf.z; nfv[3] = nf.w;
+              const uint4 w4 = nfq[b * QB + qq];
+              m[0] = w4.x; m[1] = w4.y; m[2] = w4.z; m[3] = w4.w;
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint32_t t = tin & nfv[k];
-              const uint32_t d = __vmaxu2(V[4 * q + k], t);
-              V[4 * q + k] = V[4 * q + k] ^ tin ^ d;
-              tin = d;
+              uint32_t& v = V[b * RB + 4 * qq + k];
+              uint32_t tt;
+              if constexpr (XM) {
+                tt = t & m[k];
+              } else {
+                asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(tt) : "r"(t), "r"(m[k]), "r"(zero));
+              }
+              const uint32_t d = __vmaxu2(v, tt);
+              v = lop3_xor(v, t, d);
+              t = d;
             }
           }
-          tout = tin;
-          if (j == L - 1) ringB[sub * 8 + u] = tout;
-          yprev = yc;
+          tb[b] = t;
         }
-        ycur = ynext;
+        if (j == L - 1) ringB[u] = tb[K - 1];
+        // codes of the next step: band b takes band b-1's, band 0 lane j-1's last band's
+        {
+          const uint32_t un = u + 1;
+          const uint32_t ynew = un < kChunk ? (yc_words[un >> 2] >> (8 * (un & 3))) & 0xFFu : nxa.x & 0xFFu;
+          const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, cd[K - 1], 1, L);
+#pragma unroll
+          for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
+          cd[0] = j == 0 ? ynew : sh;
+        }
       }
+      ych = nxa;
+      ych2 = nxb;
       __syncwarp();
 
-      // ---- window extraction for bottom columns [E0, E0 + 32)
-      const int32_t E0 = int32_t(ch * kChunk) - (L - 1);
-#pragma unroll 1
-      for (int rd = 0; rd < kChunk / L; ++rd) {
-        const int32_t e = E0 + rd * L + int32_t(j);
+      // ---- window extraction for bottom columns [E0, E0 + 32); lane j owns the
+      //   CPL consecutive columns E0 + j*CPL + c.  Per column e with bottom key k:
+      //   countable iff span < W; then the seaweed's start st gets an ok flag, and
+      //   count(K+1) = count(K) + [e = K+W countable] - ok[K]   (K = e - W).
+      constexpr int CPL = kChunk / L;
+      const int32_t E0 = int32_t(ch * kChunk) - (VB - 1);
+      const int32_t eb = E0 + int32_t(j) * CPL;
+      uint32_t cmask = 0;   // bit 2c: strip A countable, bit 2c+1: strip B
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int32_t e = eb + c;
         const bool valid = e >= 0 && e < int32_t(nseg_cols);
-        const uint32_t k = ringB[rd * L + j];
+        const uint32_t k = ringB[j * CPL + c];
         const int32_t thr = e - kbase - int32_t(p.W);
         const int32_t kA = int32_t(k & 0xFFFFu), kB = int32_t(k >> 16);
         const bool cA = valid && kA > thr;
         const bool cB = valid && kB > thr;
         if (cA) okA[uint32_t(kA + kbase) & rmask] = 1;
         if (cB) okB[uint32_t(kB + kbase) & rmask] = 1;
-        __syncwarp();
+        cmask |= (uint32_t(cA) | (uint32_t(cB) << 1)) << (2 * c);
+      }
+      __syncwarp();
+      uint32_t dl[CPL];
+      uint32_t acc = 0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int32_t e = eb + c;
+        const bool valid = e >= 0 && e < int32_t(nseg_cols);
         uint32_t oA = 0, oB = 0;
         if (valid) {
           const uint32_t slot = uint32_t(e - int32_t(p.W)) & rmask;
@@ -251,62 +331,95 @@ comb_kernel(const CombParams p) {
           okA[slot] = 0;
           okB[slot] = 0;
         }
-        uint32_t dl = (uint32_t(cA) + 1u - oA) | ((uint32_t(cB) + 1u - oB) << 16);
+        const uint32_t cA = (cmask >> (2 * c)) & 1u, cB = (cmask >> (2 * c + 1)) & 1u;
+        acc += (cA + 1u - oA) | ((cB + 1u - oB) << 16);   // biased by +1 per half
+        dl[c] = acc;
+      }
+      // exclusive scan of the lane totals across the group
+      uint32_t incl = acc;
 #pragma unroll
-        for (int off = 1; off < L; off <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, dl, off, L);
-          if (j >= uint32_t(off)) dl += v;
-        }
-        const uint32_t cnt = run + dl - (j + 1) * 0x00010001u;
-        run = __shfl_sync(0xFFFFFFFFu, cnt, L - 1, L);
-
+      for (int off = 1; off < L; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off, L);
+        if (j >= uint32_t(off)) incl += v;
+      }
+      const uint32_t excl = incl - acc;
+      const uint32_t bias0 = j * CPL * 0x00010001u;
+      uint32_t hmA = 0, hmB = 0;      // threshold hits of this lane's columns (bit c)
+      uint32_t hv[DENSE ? 1 : CPL];   // packed half-unit scores hA | hB << 16
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int32_t e = eb + c;
+        const bool valid = e >= 0 && e < int32_t(nseg_cols);
+        const uint32_t cnt = run + excl + dl[c] - bias0 - uint32_t(c + 1) * 0x00010001u;
         const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
-        const bool out_ok = valid && kp >= 0 && kp < int32_t(p.S) && (p.r == 1 || !(kp & 1));
-        const uint32_t gcol = (c0 + uint32_t(kp)) / p.r;
+        const bool out_ok = valid && kp >= 0 && kp < int32_t(p.S) && !(uint32_t(kp) & rshift);
+        const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
         const int32_t llA = int32_t(p.W) - int32_t(cnt & 0xFFFFu);
         const int32_t llB = int32_t(p.W) - int32_t(cnt >> 16);
-        const int32_t hA = p.r == 1 ? 2 * llA : 2 * llA - 2 * int32_t(p.w);
-        const int32_t hB = p.r == 1 ? 2 * llB : 2 * llB - 2 * int32_t(p.w);
+        const int32_t hA = 2 * llA - (rshift ? 2 * int32_t(p.w) : 0);
+        const int32_t hB = 2 * llB - (rshift ? 2 * int32_t(p.w) : 0);
         if constexpr (DENSE) {
           if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
           if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
         } else {
-          const bool hitA = out_ok && hasA && hA >= p.t_half;
-          const bool hitB = out_ok && hasB && hB >= p.t_half;
-          const uint32_t bA = __ballot_sync(0xFFFFFFFFu, hitA);
-          const uint32_t bB = __ballot_sync(0xFFFFFFFFu, hitB);
-          if (bA | bB) {
-            const uint32_t gmask = (L == 32 ? 0xFFFFFFFFu : ((1u << L) - 1u)) << (g * L);
-            const uint32_t lt = (1u << lane) - 1u;
-            const uint32_t total = __popc(bA) + __popc(bB);
-            unsigned long long basepos = 0;
-            if (lane == 0) basepos = atomicAdd(p.cursor, (unsigned long long)total);
-            basepos = __shfl_sync(0xFFFFFFFFu, basepos, 0);
-            if (hitA) {
-              const unsigned long long pos = basepos + __popc(bA & lt);
-              const uint32_t rank = hitsA + __popc(bA & gmask & lt);
-              if (pos < p.stage_cap)
-                p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, uint32_t(hA), rank);
-            }
-            if (hitB) {
-              const unsigned long long pos = basepos + __popc(bA) + __popc(bB & lt);
-              const uint32_t rank = hitsB + __popc(bB & gmask & lt);
-              if (pos < p.stage_cap)
-                p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, uint32_t(hB), rank);
-            }
-            hitsA += __popc(bA & gmask);
-            hitsB += __popc(bB & gmask);
-          }
+          hmA |= uint32_t(out_ok && hasA && hA >= p.t_half) << c;
+          hmB |= uint32_t(out_ok && hasB && hB >= p.t_half) << c;
+          hv[c] = uint32_t(hA) | (uint32_t(hB) << 16);
         }
-        __syncwarp();
       }
+      if constexpr (!DENSE) {
+        // Row-major ranks: a hit's rank in its (row, segment) = the row's earlier
+        // hits (previous chunks, lower lanes of this chunk, lower columns of this lane).
+        if (__any_sync(0xFFFFFFFFu, hmA | hmB)) {
+          const uint32_t nA = __popc(hmA), nB = __popc(hmB);
+          const uint32_t pk = nA | (nB << 16);
+          uint32_t gi = pk;
+#pragma unroll
+          for (int off = 1; off < L; off <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, gi, off, L);
+            if (j >= uint32_t(off)) gi += v;
+          }
+          const uint32_t gex = gi - pk;
+          const uint32_t gtot = __shfl_sync(0xFFFFFFFFu, gi, L - 1, L);
+          uint32_t wi = nA + nB;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, off);
+            if (lane >= uint32_t(off)) wi += v;
+          }
+          const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, wi, 31);
+          unsigned long long pos = 0;
+          if (lane == 0) pos = atomicAdd(p.cursor, (unsigned long long)wtot);
+          pos = __shfl_sync(0xFFFFFFFFu, pos, 0) + (wi - nA - nB);
+          uint32_t rkA = hitsA + (gex & 0xFFFFu), rkB = hitsB + (gex >> 16);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint32_t gcol = (c0 + uint32_t(eb + c - int32_t(p.W) + 1)) >> rshift;
+            if ((hmA >> c) & 1u) {
+              if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hv[c] & 0xFFFFu, rkA);
+              ++pos;
+              ++rkA;
+            }
+            if ((hmB >> c) & 1u) {
+              if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hv[c] >> 16, rkB);
+              ++pos;
+              ++rkB;
+            }
+          }
+          hitsA += gtot & 0xFFFFu;
+          hitsB += gtot >> 16;
+        }
+      }
+      run = __shfl_sync(0xFFFFFFFFu, run + incl - (j + 1) * CPL * 0x00010001u, L - 1, L);
+      __syncwarp();
 
-      // ---- key rebase (saturating at 0): keeps fresh keys below 2^16
-      if (uint32_t(int32_t((ch + 1) * kChunk + kChunk) - kbase) >= kRebaseAt) {
+      // ---- key rebase (saturating at 0): fresh keys stay below 0x7BFF (fp16-finite)
+      if (uint32_t(int32_t((ch + 2) * kChunk) - kbase) >= kRebaseAt) {
         const uint32_t by = kRebaseBy * 0x00010001u;
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) V[rho] = __vmaxu2(V[rho], by) - by;
-        tout = __vmaxu2(tout, by) - by;
+#pragma unroll
+        for (int b = 0; b < K; ++b) tb[b] = __vmaxu2(tb[b], by) - by;
         fresh -= by;
         kbase += int32_t(kRebaseBy);
       }

@@ -1,134 +1,150 @@
-// Integer-pipe issue-rate microbenchmark for the roofline denominator
-// (P_int = N_SM x int32 ops/clk/SM x clock).
-// Each kernel runs 8 independent dependency chains of one SASS op per thread;
-// ops/clk/SM is computed from per-CTA clock64 deltas, so it is clock-free.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o int_peak int_peak.cu
-#include <cstdio>
-#include <cstdint>
+// Integer / fp16-pipe issue-rate microbenchmark: the roofline denominator
+// (P_int = N_SM x int32 lane-ops/clk/SM x clock) and the
+// pipe assignment of the ops the comb kernel can use.
+// Each kernel runs CH independent dependency chains per thread (per-chain
+// operand registers, asm volatile, chains that cannot fold).  Rates are
+// lane-ops per SM-clock over the SM-wide span (min start .. max end of the
+// CTAs resident on that SM, from %smid + clock64), so they are clock-free.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o int_peak.bin int_peak.cu
 #include <cuda_fp16.h>
+#include <cstdint>
+#include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <map>
 
-#define ITERS 4096
-#define CHAINS 8
+#define ITERS 1024
+#define CH 16
 
-struct Rec { long long t0, t1; };
+struct Rec { long long t0, t1; int sm; };
 
-template <int OP>
-__device__ __forceinline__ uint32_t op(uint32_t a, uint32_t b, uint32_t c, int parity) {
-  if constexpr (OP == 0) {  // LOP3
-    uint32_t d; asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d;
-  } else if constexpr (OP == 1) {  // IADD3
-    return a + b + c;
-  } else if constexpr (OP == 2) {  // VIMNMX.U16x2 (alternate max / min so nothing folds)
-    return parity ? __vmaxu2(a, b) : __vminu2(a, b);
-  } else if constexpr (OP == 3) {  // VIADDMNMX.U16x2
-    return parity ? __viaddmax_u16x2(a, b, c) : __viaddmin_u16x2(a, b, c);
-  } else if constexpr (OP == 4) {  // PRMT
-    return __byte_perm(a, b, c);
-  } else if constexpr (OP == 5) {  // HMNMX2
-    __half2 x = *reinterpret_cast<__half2*>(&a), y = *reinterpret_cast<__half2*>(&b);
-    __half2 r = parity ? __hmax2(x, y) : __hmin2(x, y); return *reinterpret_cast<uint32_t*>(&r);
-  } else if constexpr (OP == 6) {  // HMUL2
-    __half2 x = *reinterpret_cast<__half2*>(&a), y = *reinterpret_cast<__half2*>(&b);
-    __half2 r = __hmul2(x, y); return *reinterpret_cast<uint32_t*>(&r);
-  } else if constexpr (OP == 7) {  // IMAD
-    return a * b + c;
-  } else {  // 8: the comb cell triple: D = max(V, T & NF); R = V ^ T ^ D
-    uint32_t t = b & c;
-    uint32_t d = __vmaxu2(a, t);
-    return a ^ b ^ d;
-  }
+__device__ __forceinline__ uint32_t smid() { uint32_t s; asm volatile("mov.u32 %0, %%smid;" : "=r"(s)); return s; }
+
+#define LOP3(d, a, b, c) asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c))
+#define VMAX(d, a, b) asm volatile("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
+#define VMIN(d, a, b) asm volatile("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
+#define IMAD(d, a, b, c) asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c))
+#define PRMT(d, a, b, c) asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c))
+#define HMUL(d, a, b) asm volatile("mul.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
+#define HMAX(d, a, b) asm volatile("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
+#define HMIN(d, a, b) asm volatile("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
+#define HFMA(d, a, b, c) asm volatile("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c))
+
+// Each VARIANT body updates v[i] with K ops (K returned by kops()).
+template <int V> __host__ __device__ constexpr int kops() {
+  return V == 0 ? 1 : V == 1 ? 2 : V == 2 ? 1 : V == 3 ? 1 : V == 4 ? 2 : V == 5 ? 1 : V == 6 ? 2 : V == 7 ? 2 : V == 8 ? 2 : V == 9 ? 3 : V == 10 ? 3 : V == 11 ? 3 : 2;
 }
 
-template <int OP>
+template <int V>
 __global__ void k_ops(uint32_t* out, Rec* rec, uint32_t seed) {
-  uint32_t v[CHAINS];
-  uint32_t b = seed ^ threadIdx.x, c = seed * 3u + blockIdx.x;
+  uint32_t v[CH], b[CH], c[CH];
 #pragma unroll
-  for (int i = 0; i < CHAINS; ++i) v[i] = seed + i * 77u + threadIdx.x;
-  __syncthreads();
-  long long t0 = clock64();
-  for (int it = 0; it < ITERS; ++it) {
-#pragma unroll
-    for (int i = 0; i < CHAINS; ++i) v[i] = op<OP>(v[i], v[(i + 1) % CHAINS], (OP == 4 ? (b + i) & 0x7777u : c), 1);
-#pragma unroll
-    for (int i = 0; i < CHAINS; ++i) v[i] = op<OP>(v[i], v[(i + 3) % CHAINS], (OP == 4 ? (c + i) & 0x7777u : b), 0);
+  for (int i = 0; i < CH; ++i) {
+    v[i] = (seed * (i + 3) + threadIdx.x) & 0x3BFF3BFFu;
+    b[i] = ((seed ^ (i * 0x9E3779B9u)) & 0x3BFF3BFFu) | 0x3C003C00u;
+    c[i] = ((seed + i) * 0x85EBCA6Bu) & 0x3BFF3BFFu;
   }
   __syncthreads();
-  long long t1 = clock64();
-  uint32_t acc = 0;
-#pragma unroll
-  for (int i = 0; i < CHAINS; ++i) acc ^= v[i];
-  if (acc == 0x12345678u) out[0] = acc;
-  if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1};
-}
-
-__global__ void k_shfl(uint32_t* out, Rec* rec, uint32_t seed) {
-  uint32_t v[CHAINS];
-#pragma unroll
-  for (int i = 0; i < CHAINS; ++i) v[i] = seed + i + threadIdx.x;
-  __syncthreads();
   long long t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
-    for (int i = 0; i < CHAINS; ++i) v[i] = __shfl_up_sync(0xffffffffu, v[i], 1, 8);
-#pragma unroll
-    for (int i = 0; i < CHAINS; ++i) v[i] = __shfl_up_sync(0xffffffffu, v[i], 1, 8);
-  }
-  __syncthreads();
-  long long t1 = clock64();
-  uint32_t acc = 0;
-  for (int i = 0; i < CHAINS; ++i) acc ^= v[i];
-  if (acc == 0x12345678u) out[0] = acc;
-  if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1};
-}
-
-__global__ void k_lds128(uint32_t* out, Rec* rec, uint32_t seed) {
-  __shared__ uint4 tab[2048];
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) tab[i] = make_uint4(i, i + 1, i + 2, (i * 7) & 3);
-  __syncthreads();
-  uint32_t idx = (seed + threadIdx.x) & 3;
-  uint32_t acc = 0;
-  long long t0 = clock64();
-  for (int it = 0; it < ITERS; ++it) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      uint4 q = tab[(idx * 512 + (threadIdx.x & 31) + i * 32) & 2047];
-      acc += q.x ^ q.y ^ q.z; idx = q.w;
+    for (int i = 0; i < CH; ++i) {
+      uint32_t d, e, f;
+      if constexpr (V == 0) { LOP3(d, v[i], b[i], c[i]); v[i] = d; }              // alu
+      if constexpr (V == 1) { VMAX(d, v[i], b[i]); VMIN(e, d, c[i]); v[i] = e; }  // alu alu
+      if constexpr (V == 2) { IMAD(d, v[i], b[i], c[i]); v[i] = d; }             // fma
+      if constexpr (V == 3) { PRMT(d, v[i], b[i], c[i]); v[i] = d; }
+      if constexpr (V == 4) { HMAX(d, v[i], b[i]); HMIN(e, d, c[i]); v[i] = e; }
+      if constexpr (V == 5) { HMUL(d, v[i], b[i]); v[i] = d; }
+      if constexpr (V == 6) { LOP3(d, v[i], b[i], c[i]); IMAD(e, d, b[i], c[i]); v[i] = e; }
+      if constexpr (V == 7) { LOP3(d, v[i], b[i], c[i]); HMUL(e, d, b[i]); v[i] = e; }
+      if constexpr (V == 8) { VMAX(d, v[i], b[i]); HMIN(e, d, c[i]); v[i] = e; }
+      // comb cell (table): t = T & NF; d = max(V, t); V' = V ^ T ^ d      [alu, alu, alu]
+      if constexpr (V == 9) { uint32_t t = v[(i + CH - 1) % CH]; asm volatile("and.b32 %0, %1, %2;" : "=r"(d) : "r"(t), "r"(b[i])); VMAX(e, v[i], d); LOP3(f, v[i], t, e); v[i] = f; }
+      // comb cell (fp16 key): t = T * M (HMUL2); d = max(V, t) (VIMNMX); V' = V ^ T ^ d   [fma?, alu, alu]
+      if constexpr (V == 10) { uint32_t t = v[(i + CH - 1) % CH]; HMUL(d, t, b[i]); VMAX(e, v[i], d); LOP3(f, v[i], t, e); v[i] = f; }
+      // comb cell (fp16 key, fp16 max): HMUL2, HMNMX2, LOP3
+      if constexpr (V == 11) { uint32_t t = v[(i + CH - 1) % CH]; HMUL(d, t, b[i]); HMAX(e, v[i], d); LOP3(f, v[i], t, e); v[i] = f; }
+      if constexpr (V == 12) { HFMA(d, v[i], b[i], c[i]); LOP3(e, d, b[i], c[i]); v[i] = e; }
     }
   }
   __syncthreads();
   long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) acc ^= v[i];
   if (acc == 0x12345678u) out[0] = acc;
-  if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1};
+  if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1, (int)smid()};
+}
+
+// fp16 bit-pattern semantics the fp16-key comb relies on (no FTZ, exact x*1, x*0 = +0,
+// max/min of positive finite halves == unsigned max/min of their bit patterns).
+__global__ void k_check(uint32_t* bad) {
+  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a <= 0x7BFFu; a += gridDim.x * blockDim.x) {
+    const uint32_t one = 0x3C003C00u, zero = 0u;
+    uint32_t k = a | (a << 16), d;
+    HMUL(d, k, one); if (d != k) atomicAdd(bad, 1);
+    HMUL(d, k, zero); if (d != 0) atomicAdd(bad + 1, 1);
+    for (uint32_t bb = 0; bb <= 0x7BFFu; bb += 97) {
+      uint32_t kb = bb | ((0x7BFFu - bb) << 16);
+      uint32_t ka = a | (a << 16), mx, mn, vm, vn;
+      HMAX(mx, ka, kb); HMIN(mn, ka, kb);
+      VMAX(vm, ka, kb); VMIN(vn, ka, kb);
+      if (mx != vm) atomicAdd(bad + 2, 1);
+      if (mn != vn) atomicAdd(bad + 3, 1);
+    }
+  }
 }
 
 int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   const int nsm = p.multiProcessorCount;
-  const int threads = 256, per_sm = 4, blocks = nsm * per_sm;
-  uint32_t* out; Rec* rec; cudaMalloc(&out, 4); cudaMalloc(&rec, blocks * sizeof(Rec));
-  std::vector<Rec> h(blocks);
-  auto report = [&](const char* name, double ops_per_thread) {
+  uint32_t* out; Rec* rec; cudaMalloc(&out, 64); cudaMalloc(&rec, 64 * nsm * sizeof(Rec));
+  std::vector<Rec> h(64 * nsm);
+  auto run = [&](auto kern, const char* name, int warps_per_sm, int k) {
+    const int threads = 128;
+    const int blocks = nsm * warps_per_sm / 4;
+    kern<<<blocks, threads>>>(out, rec, 7);
+    kern<<<blocks, threads>>>(out, rec, 7);
     cudaDeviceSynchronize();
     cudaMemcpy(h.data(), rec, blocks * sizeof(Rec), cudaMemcpyDeviceToHost);
-    // all blocks resident at once (4 x 256 threads per SM): cycles = median CTA span
-    std::vector<double> d; for (auto& r : h) d.push_back(double(r.t1 - r.t0));
-    std::sort(d.begin(), d.end());
-    double cyc = d[d.size() / 2];
-    double per_sm_ops = ops_per_thread * threads * per_sm;
-    printf("{\"op\": \"%s\", \"lane_ops_per_clk_per_sm\": %.2f, \"cycles\": %.0f}\n", name, per_sm_ops / cyc, cyc);
+    std::map<int, std::pair<long long, long long>> span;
+    std::map<int, int> nblk;
+    for (int i = 0; i < blocks; ++i) {
+      auto it = span.find(h[i].sm);
+      if (it == span.end()) span[h[i].sm] = {h[i].t0, h[i].t1};
+      else { it->second.first = std::min(it->second.first, h[i].t0); it->second.second = std::max(it->second.second, h[i].t1); }
+      nblk[h[i].sm]++;
+    }
+    std::vector<double> rates;
+    for (auto& kv : span) rates.push_back(double(nblk[kv.first]) * threads * double(k) * CH * ITERS / double(kv.second.second - kv.second.first));
+    std::sort(rates.begin(), rates.end());
+    const double r = rates[rates.size() / 2];
+    printf("{\"op\": \"%s\", \"warps_per_sm\": %d, \"lane_ops_per_clk_per_sm\": %.2f}\n", name, warps_per_sm, r);
+    return r;
   };
-  const double ops = 2.0 * ITERS * CHAINS;
-#define RUN(OP, NAME, MULT) k_ops<OP><<<blocks, threads>>>(out, rec, 1); report(NAME, ops * MULT);
-  for (int rep = 0; rep < 2; ++rep) {
-    RUN(0, "LOP3", 1) RUN(1, "IADD3", 1) RUN(2, "VIMNMX.U16x2", 1) RUN(3, "VIADDMNMX.U16x2", 1)
-    RUN(4, "PRMT", 1) RUN(5, "HMNMX2", 1) RUN(6, "HMUL2", 1) RUN(7, "IMAD", 1) RUN(8, "comb_triple(3 ops)", 3)
-    k_shfl<<<blocks, threads>>>(out, rec, 1); report("SHFL", ops);
-    k_lds128<<<blocks, threads>>>(out, rec, 1); report("LDS.128", 16.0 * ITERS);
+  double best_alu = 0;
+  for (int wps : {8, 16, 32}) {
+    best_alu = std::max(best_alu, run(k_ops<0>, "LOP3", wps, kops<0>()));
+    best_alu = std::max(best_alu, run(k_ops<1>, "VIMNMX.U16x2", wps, kops<1>()));
+    run(k_ops<2>, "IMAD", wps, kops<2>());
+    run(k_ops<3>, "PRMT", wps, kops<3>());
+    run(k_ops<4>, "HMNMX2", wps, kops<4>());
+    run(k_ops<5>, "HMUL2", wps, kops<5>());
+    run(k_ops<6>, "LOP3+IMAD", wps, kops<6>());
+    run(k_ops<7>, "LOP3+HMUL2", wps, kops<7>());
+    run(k_ops<8>, "VIMNMX+HMNMX2", wps, kops<8>());
+    run(k_ops<12>, "HFMA2+LOP3", wps, kops<12>());
+    run(k_ops<9>, "cell(AND,VIMNMX,LOP3)", wps, kops<9>());
+    run(k_ops<10>, "cell(HMUL2,VIMNMX,LOP3)", wps, kops<10>());
+    run(k_ops<11>, "cell(HMUL2,HMNMX2,LOP3)", wps, kops<11>());
   }
+  uint32_t* bad; cudaMalloc(&bad, 16); cudaMemset(bad, 0, 16);
+  k_check<<<256, 128>>>(bad);
+  uint32_t hb[4]; cudaMemcpy(hb, bad, 16, cudaMemcpyDeviceToHost);
+  printf("{\"fp16_check\": {\"mul_one_bad\": %u, \"mul_zero_bad\": %u, \"max_bad\": %u, \"min_bad\": %u}}\n", hb[0], hb[1], hb[2], hb[3]);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"name\": \"%s\"}\n", nsm, clk, p.name);
+  printf("{\"summary\": true, \"sms\": %d, \"clock_khz_attr\": %d, \"alu_lane_ops_per_clk_per_sm\": %.2f, \"name\": \"%s\"}\n",
+         nsm, clk, best_alu, p.name);
   return 0;
 }
