@@ -1,25 +1,30 @@
 # Top-level build: the CUDA engine (sm_100a) and the oracle checkers.
-#   make            -> paper_0909_2000_b200/libalignplot_b200.so + oracle/
+#   make -j4        -> paper_0909_2000_b200/libalignplot_b200.so + oracle/
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
 PKG := paper_0909_2000_b200
+CSRC := $(PKG)/csrc
 LIB := $(PKG)/libalignplot_b200.so
-SRCS := $(PKG)/csrc/ap_capi.cu
-HDRS := $(PKG)/csrc/ap_kernels.cuh include/alignplot_b200.h
+OBJS := build/ap_capi.o build/ap_inst_l8.o build/ap_inst_l16.o build/ap_inst_l32.o
+HDRS := $(CSRC)/ap_kernels.cuh $(CSRC)/ap_aux_kernels.cuh include/alignplot_b200.h
 
 all: $(LIB) oracle
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build/ptxas.log || (cat build/ptxas.log; false)
+build/%.o: $(CSRC)/%.cu $(HDRS) | build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+build:
+	mkdir -p build
 
 oracle:
 	$(MAKE) -C oracle
 
-$(shell mkdir -p build)
-
 clean:
-	rm -f $(LIB)
+	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

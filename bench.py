@@ -71,7 +71,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -273,6 +273,7 @@ def run_engine(args, rank, world, local_rank):
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)
+            evs[i][1].synchronize()   # so the comb-kernel events of this step can be read
             kern_ms.append(L.ap_ctx_last_kernel_ms(ctx))
             launches += L.ap_ctx_last_launches(ctx)
         torch.cuda.synchronize()
@@ -385,8 +386,8 @@ def run_engine(args, rank, world, local_rank):
 def main():
     ap_ = argparse.ArgumentParser()
     ap_.add_argument("--gpus", type=int, default=1)
-    ap_.add_argument("--steps", type=int, default=10)
-    ap_.add_argument("--warmup", type=int, default=3)
+    ap_.add_argument("--steps", type=int, default=30)
+    ap_.add_argument("--warmup", type=int, default=5)
     ap_.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS))
     ap_.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap_.add_argument("--ref-seconds", type=float, default=8.0, help="wall-clock budget of the CPU reference sample")

@@ -1,0 +1,72 @@
+// ap_aux_kernels.cuh — the small kernels around the comb kernel (included by
+// ap_capi.cu only): code streams (fused $-interleave), alphabet mapping and the
+// deterministic placement of thresholded records.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace apk {
+
+// K1: effective y code stream (fused $-interleave, scoring.cpp:5-17):
+// ycode[c] = r == 2 ? (c odd ? map[y[c/2]] : sent) : map[y[c]]; pad with 0.
+__global__ void ycode_kernel(const uint8_t* __restrict__ y, size_t n, uint32_t r, uint32_t sent,
+                             const uint8_t* __restrict__ map, uint8_t* __restrict__ ycode,
+                             size_t total) {
+  for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < total;
+       c += size_t(gridDim.x) * blockDim.x) {
+    const size_t N = n * r;
+    uint8_t v = 0;
+    if (c < N) v = (r == 2) ? ((c & 1) ? map[y[c >> 1]] : uint8_t(sent)) : map[y[c]];
+    ycode[c] = v;
+  }
+}
+
+// x codes: map[x[i]] (0xFF for bytes absent from y).
+__global__ void xcode_kernel(const uint8_t* __restrict__ x, size_t m, const uint8_t* __restrict__ map,
+                             uint8_t* __restrict__ xcode) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < m;
+       i += size_t(gridDim.x) * blockDim.x)
+    xcode[i] = map[x[i]];
+}
+
+// Alphabet of y: presence bitmap -> dense codes (map[b] = rank of b among the
+// bytes present in y, 0xFF if absent), sigma -> out[256].  One CTA.
+__global__ void alphabet_kernel(const uint8_t* __restrict__ y, size_t n, uint8_t* __restrict__ map,
+                                uint32_t* __restrict__ sigma_out, uint32_t* __restrict__ zero_flag) {
+  __shared__ uint32_t present[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) present[b] = 0;
+  __syncthreads();
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) present[y[i]] = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t k = 0;
+    for (int b = 0; b < 256; ++b) {
+      map[b] = present[b] ? uint8_t(k) : uint8_t(0xFF);
+      k += present[b];
+    }
+    *sigma_out = k;
+    *zero_flag = present[0];
+  }
+}
+
+// Deterministic row-major placement of staged threshold records:
+// final index = offset[row * nseg + seg] + rank.
+__global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long nrec,
+                             const unsigned long long* __restrict__ offsets, uint32_t nseg,
+                             uint32_t seg_cols, uint32_t r, uint32_t row_global0,
+                             uint32_t* __restrict__ orow, uint32_t* __restrict__ ocol,
+                             uint16_t* __restrict__ ohalf, unsigned long long cap) {
+  for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < nrec;
+       i += 1ull * gridDim.x * blockDim.x) {
+    const uint4 rec = stage[i];
+    const uint32_t seg = (rec.y * r) / seg_cols;
+    const unsigned long long pos = offsets[size_t(rec.x - row_global0) * nseg + seg] + rec.w;
+    if (pos < cap) {
+      orow[pos] = rec.x;
+      ocol[pos] = rec.y;
+      ohalf[pos] = uint16_t(rec.z);
+    }
+  }
+}
+
+}  // namespace apk

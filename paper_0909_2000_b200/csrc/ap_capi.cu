@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "../../include/alignplot_b200.h"
+#include "ap_aux_kernels.cuh"
 #include "ap_kernels.cuh"
 
 namespace {
@@ -47,31 +49,21 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // ---- kernel shape table ---------------------------------------------------
-using KernelFn = void (*)(apk::CombParams);
-constexpr int kBands = 2;
+using apk::KernelFn;
 
-template <int L, int R, bool XM>
-KernelFn pick_fn(bool dense) {
-  return dense ? reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, kBands, true, XM>)
-               : reinterpret_cast<KernelFn>(&apk::comb_kernel<L, R, kBands, false, XM>);
-}
+// Instantiated shapes: (L lanes per strip pair, R rows per lane, K bands per lane).
+struct ShapeDef { int L, R, K; };
+constexpr ShapeDef kShapes[] = {
+    {8, 8, 2},  {8, 16, 2},  {8, 16, 4},  {8, 24, 2},  {8, 32, 2},  {8, 32, 4},
+    {16, 8, 2}, {16, 16, 2}, {16, 16, 4}, {16, 24, 2}, {16, 32, 2}, {16, 32, 4},
+    {32, 8, 2}, {32, 16, 2}, {32, 16, 4}, {32, 24, 2}, {32, 32, 2}, {32, 32, 4},
+};
 
-template <int L>
-KernelFn pick_r(int R, bool dense, bool xm) {
-  switch (R) {
-    case 8: return xm ? pick_fn<L, 8, true>(dense) : pick_fn<L, 8, false>(dense);
-    case 16: return xm ? pick_fn<L, 16, true>(dense) : pick_fn<L, 16, false>(dense);
-    case 24: return xm ? pick_fn<L, 24, true>(dense) : pick_fn<L, 24, false>(dense);
-    case 32: return xm ? pick_fn<L, 32, true>(dense) : pick_fn<L, 32, false>(dense);
-  }
-  return nullptr;
-}
-
-KernelFn pick_kernel(int L, int R, bool dense, bool xm) {
-  switch (L) {
-    case 8: return pick_r<8>(R, dense, xm);
-    case 16: return pick_r<16>(R, dense, xm);
-    case 32: return pick_r<32>(R, dense, xm);
+KernelFn pick_kernel(int l, int r, int k, bool dense, bool xm) {
+  switch (l) {
+    case 8: return apk::pick_l8(r, k, dense, xm);
+    case 16: return apk::pick_l16(r, k, dense, xm);
+    case 32: return apk::pick_l32(r, k, dense, xm);
   }
   return nullptr;
 }
@@ -85,7 +77,7 @@ uint32_t next_pow2(uint32_t v) {
 }
 
 struct Shape {
-  int L = 0, R = 0;
+  int L = 0, R = 0, K = 2;
   bool xm = false;   // masks computed in registers (no table)
   uint32_t ring = 0;
   size_t smem = 0;
@@ -97,36 +89,47 @@ struct Shape {
 // 16 warps per SM fit (registers from the compiled kernel, table in shared memory).
 bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
   const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
+  // tuning override: AP_SHAPE="L,R,K[,xm]"
+  if (const char* env = std::getenv("AP_SHAPE")) {
+    int l = 0, r = 0, k = 0, xm = 0;
+    if (std::sscanf(env, "%d,%d,%d,%d", &l, &r, &k, &xm) >= 3 && pick_kernel(l, r, k, dense, xm) &&
+        uint32_t(l * r) >= W) {
+      out->L = l; out->R = r; out->K = k; out->xm = xm; out->ring = ring;
+      out->smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(l, r, xm ? 0 : sigma, ring);
+      out->warps_per_sm = 0;
+      return out->smem <= kSmemPerSm - 1024;
+    }
+  }
   double best = 1e30;
   for (int xm = 0; xm < 2; ++xm) {
-    for (int L : {8, 16, 32}) {
-      for (int R : {8, 16, 24, 32}) {
-        if (uint32_t(L * R) < W) continue;
-        KernelFn fn = pick_kernel(L, R, dense, xm);
-        if (!fn) continue;
-        cudaFuncAttributes fa;
-        if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)) != cudaSuccess) {
-          cudaGetLastError();
-          continue;
-        }
-        const size_t smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(L, R, xm ? 0 : sigma, ring);
-        if (smem > kSmemPerSm - 1024) continue;
-        const int by_regs = 65536 / (std::max(fa.numRegs, 1) * 32 * apk::kWarpsPerCta);
-        const int by_smem = int(kSmemPerSm / (smem + 1024));
-        const int ctas = std::min({by_regs, by_smem, 16});
-        if (ctas < 1) continue;
-        const int warps = ctas * apk::kWarpsPerCta;
-        double cost = double(L) * ((xm ? 6.0 : 3.0) * R + 14.0) + 25.0;
-        if (warps < 16) cost *= 16.0 / warps;
-        if (cost < best) {
-          best = cost;
-          out->L = L;
-          out->R = R;
-          out->xm = xm;
-          out->ring = ring;
-          out->smem = smem;
-          out->warps_per_sm = warps;
-        }
+    for (const ShapeDef& d : kShapes) {
+      if (uint32_t(d.L * d.R) < W) continue;
+      KernelFn fn = pick_kernel(d.L, d.R, d.K, dense, xm);
+      if (!fn) continue;
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      const size_t smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(d.L, d.R, xm ? 0 : sigma, ring);
+      if (smem > kSmemPerSm - 1024) continue;
+      const int by_regs = 65536 / (std::max(fa.numRegs, 1) * 32 * apk::kWarpsPerCta);
+      const int by_smem = int(kSmemPerSm / (smem + 1024));
+      const int ctas = std::min({by_regs, by_smem, 16});
+      if (ctas < 1) continue;
+      const int warps = ctas * apk::kWarpsPerCta;
+      double cost = double(d.L) * ((xm ? 6.0 : 3.0) * d.R + 14.0) + 25.0;
+      if (warps < 16) cost *= 16.0 / warps;
+      cost *= d.K == 4 ? 0.95 : 1.0;   // 4 bands: more ILP per lane (measured ~5% faster)
+      if (cost < best) {
+        best = cost;
+        out->L = d.L;
+        out->R = d.R;
+        out->K = d.K;
+        out->xm = xm;
+        out->ring = ring;
+        out->smem = smem;
+        out->warps_per_sm = warps;
       }
     }
   }
@@ -284,7 +287,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   CK(cudaGetLastError());
   c->last_launches += 3;
 
-  KernelFn fn = pick_kernel(sh.L, sh.R, dense, sh.xm);
+  KernelFn fn = pick_kernel(sh.L, sh.R, sh.K, dense, sh.xm);
   if (!fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", sh.L, sh.R);
   CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem)));
@@ -296,6 +299,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   // column segments: enough independent (strip pair, segment) tasks for ~4
   // waves, each segment at least 4 windows wide to bound the W-1 overlap.
   const int G = 32 / sh.L;
+  const size_t VB = size_t(sh.L) * sh.K;
+  (void)VB;
   const size_t npairs = (nrows + 1) / 2;
   const size_t ngroups = (npairs + G - 1) / G;
   const size_t out_cols_eff = (N - W) + 1;  // window starts in effective columns (stride 1)

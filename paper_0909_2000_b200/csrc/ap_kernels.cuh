@@ -73,6 +73,12 @@ struct CombParams {
   uint32_t zero;                  // always 0 (HFMA2 addend)
 };
 
+using KernelFn = void (*)(CombParams);
+// Launch-stub pointers of the instantiated comb kernels (ap_inst_l{8,16,32}.cu).
+KernelFn pick_l8(int r, int k, bool dense, bool xm);
+KernelFn pick_l16(int r, int k, bool dense, bool xm);
+KernelFn pick_l32(int r, int k, bool dense, bool xm);
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ uint32_t lop3_xor(uint32_t a, uint32_t b, uint32_t c) {
@@ -227,68 +233,75 @@ comb_kernel(const CombParams p) {
     if (j == 0) cd[0] = ych.x & 0xFFu;                 // column 0
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
-      const uint32_t yc_words[8] = {ych.x, ych.y, ych.z, ych.w, ych2.x, ych2.y, ych2.z, ych2.w};
       const uint4 nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
       const uint4 nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
+#pragma unroll 1
+      for (int sub = 0; sub < kChunk / 8; ++sub) {
+        // lane 0's codes for steps sub*8+1 .. sub*8+8 (the last from the next chunk)
+        const uint32_t w0 = sub == 0 ? ych.x : sub == 1 ? ych.z : sub == 2 ? ych2.x : ych2.z;
+        const uint32_t w1 = sub == 0 ? ych.y : sub == 1 ? ych.w : sub == 2 ? ych2.y : ych2.w;
+        const uint32_t w2 = sub == 0 ? ych.z : sub == 1 ? ych2.x : sub == 2 ? ych2.z : nxa.x;
+        uint32_t* ring_sub = ringB + sub * 8;
 #pragma unroll
-      for (int u = 0; u < kChunk; ++u) {
-        // table quads of this step (codes known since the previous step)
-        uint4 nfq[Q];
-        if constexpr (!XM) {
+        for (int u = 0; u < 8; ++u) {
+          // table quads of this step (codes known since the previous step)
+          uint4 nfq[Q];
+          if constexpr (!XM) {
 #pragma unroll
-          for (int b = 0; b < K; ++b)
+            for (int b = 0; b < K; ++b)
 #pragma unroll
-            for (int qq = 0; qq < QB; ++qq) nfq[b * QB + qq] = tl[(cd[b] * Q + b * QB + qq) * L];
-        }
-        // seaweeds entering each band
-        uint32_t tin[K];
-        {
-          const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, tb[K - 1], 1, L);
-          tin[0] = j == 0 ? fresh : sh;
-#pragma unroll
-          for (int b = 1; b < K; ++b) tin[b] = tb[b - 1];
-        }
-        fresh += 0x00010001u;
-#pragma unroll
-        for (int b = 0; b < K; ++b) {
-          uint32_t t = tin[b];
-          const uint32_t yrep = cd[b] * 0x00010001u;
-#pragma unroll
-          for (int qq = 0; qq < QB; ++qq) {
-            uint32_t m[4];
-            if constexpr (XM) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                m[k] = prmt_sign((xpair[b * RB + 4 * qq + k] ^ yrep) + 0x7FFF7FFFu, 0xBB99u);
-            } else {
-              const uint4 w4 = nfq[b * QB + qq];
-              m[0] = w4.x; m[1] = w4.y; m[2] = w4.z; m[3] = w4.w;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              uint32_t& v = V[b * RB + 4 * qq + k];
-              uint32_t tt;
-              if constexpr (XM) {
-                tt = t & m[k];
-              } else {
-                asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(tt) : "r"(t), "r"(m[k]), "r"(zero));
-              }
-              const uint32_t d = __vmaxu2(v, tt);
-              v = lop3_xor(v, t, d);
-              t = d;
-            }
+              for (int qq = 0; qq < QB; ++qq) nfq[b * QB + qq] = tl[(cd[b] * Q + b * QB + qq) * L];
           }
-          tb[b] = t;
-        }
-        if (j == L - 1) ringB[u] = tb[K - 1];
-        // codes of the next step: band b takes band b-1's, band 0 lane j-1's last band's
-        {
-          const uint32_t un = u + 1;
-          const uint32_t ynew = un < kChunk ? (yc_words[un >> 2] >> (8 * (un & 3))) & 0xFFu : nxa.x & 0xFFu;
-          const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, cd[K - 1], 1, L);
+          // seaweeds entering each band
+          uint32_t tin[K];
+          {
+            const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, tb[K - 1], 1, L);
+            tin[0] = j == 0 ? fresh : sh;
 #pragma unroll
-          for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
-          cd[0] = j == 0 ? ynew : sh;
+            for (int b = 1; b < K; ++b) tin[b] = tb[b - 1];
+          }
+          fresh += 0x00010001u;
+#pragma unroll
+          for (int b = 0; b < K; ++b) {
+            uint32_t t = tin[b];
+            const uint32_t yrep = cd[b] * 0x00010001u;
+#pragma unroll
+            for (int qq = 0; qq < QB; ++qq) {
+              uint32_t m[4];
+              if constexpr (XM) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  m[k] = prmt_sign((xpair[b * RB + 4 * qq + k] ^ yrep) + 0x7FFF7FFFu, 0xBB99u);
+              } else {
+                const uint4 w4 = nfq[b * QB + qq];
+                m[0] = w4.x; m[1] = w4.y; m[2] = w4.z; m[3] = w4.w;
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                uint32_t& v = V[b * RB + 4 * qq + k];
+                uint32_t tt;
+                if constexpr (XM) {
+                  tt = t & m[k];
+                } else {
+                  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(tt) : "r"(t), "r"(m[k]));
+                }
+                const uint32_t d = __vmaxu2(v, tt);
+                v = lop3_xor(v, t, d);
+                t = d;
+              }
+            }
+            tb[b] = t;
+          }
+          if (j == L - 1) ring_sub[u] = tb[K - 1];
+          // codes of the next step: band b takes band b-1's, band 0 lane j-1's last band's
+          {
+            const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
+            const uint32_t ynew = (ww >> (8 * ((u + 1) & 3))) & 0xFFu;
+            const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, cd[K - 1], 1, L);
+#pragma unroll
+            for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
+            cd[0] = j == 0 ? ynew : sh;
+          }
         }
       }
       ych = nxa;
@@ -429,68 +442,6 @@ comb_kernel(const CombParams p) {
         if (hasA) p.seg_counts[size_t(rA) * p.nseg + seg] = hitsA;
         if (hasB) p.seg_counts[size_t(rB) * p.nseg + seg] = hitsB;
       }
-    }
-  }
-}
-
-// K1: effective y code stream (fused $-interleave, scoring.cpp:5-17):
-// ycode[c] = r == 2 ? (c odd ? map[y[c/2]] : sent) : map[y[c]]; pad with 0.
-__global__ void ycode_kernel(const uint8_t* __restrict__ y, size_t n, uint32_t r, uint32_t sent,
-                             const uint8_t* __restrict__ map, uint8_t* __restrict__ ycode,
-                             size_t total) {
-  for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < total;
-       c += size_t(gridDim.x) * blockDim.x) {
-    const size_t N = n * r;
-    uint8_t v = 0;
-    if (c < N) v = (r == 2) ? ((c & 1) ? map[y[c >> 1]] : uint8_t(sent)) : map[y[c]];
-    ycode[c] = v;
-  }
-}
-
-// x codes: map[x[i]] (0xFF for bytes absent from y).
-__global__ void xcode_kernel(const uint8_t* __restrict__ x, size_t m, const uint8_t* __restrict__ map,
-                             uint8_t* __restrict__ xcode) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < m;
-       i += size_t(gridDim.x) * blockDim.x)
-    xcode[i] = map[x[i]];
-}
-
-// Alphabet of y: presence bitmap -> dense codes (map[b] = rank of b among the
-// bytes present in y, 0xFF if absent), sigma -> out[256].  One CTA.
-__global__ void alphabet_kernel(const uint8_t* __restrict__ y, size_t n, uint8_t* __restrict__ map,
-                                uint32_t* __restrict__ sigma_out, uint32_t* __restrict__ zero_flag) {
-  __shared__ uint32_t present[256];
-  for (int b = threadIdx.x; b < 256; b += blockDim.x) present[b] = 0;
-  __syncthreads();
-  for (size_t i = threadIdx.x; i < n; i += blockDim.x) present[y[i]] = 1;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t k = 0;
-    for (int b = 0; b < 256; ++b) {
-      map[b] = present[b] ? uint8_t(k) : uint8_t(0xFF);
-      k += present[b];
-    }
-    *sigma_out = k;
-    *zero_flag = present[0];
-  }
-}
-
-// Deterministic row-major placement of staged threshold records:
-// final index = offset[row * nseg + seg] + rank.
-__global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long nrec,
-                             const unsigned long long* __restrict__ offsets, uint32_t nseg,
-                             uint32_t seg_cols, uint32_t r, uint32_t row_global0,
-                             uint32_t* __restrict__ orow, uint32_t* __restrict__ ocol,
-                             uint16_t* __restrict__ ohalf, unsigned long long cap) {
-  for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < nrec;
-       i += 1ull * gridDim.x * blockDim.x) {
-    const uint4 rec = stage[i];
-    const uint32_t seg = (rec.y * r) / seg_cols;
-    const unsigned long long pos = offsets[size_t(rec.x - row_global0) * nseg + seg] + rec.w;
-    if (pos < cap) {
-      orow[pos] = rec.x;
-      ocol[pos] = rec.y;
-      ohalf[pos] = uint16_t(rec.z);
     }
   }
 }
