@@ -241,7 +241,9 @@ def run_engine(args, rank, world, local_rank):
         d_r = torch.empty(cap, dtype=torch.int32, device=dev)
         d_c = torch.empty(cap, dtype=torch.int32, device=dev)
         d_h = torch.empty(cap, dtype=torch.int16, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: handle 0 would mean "the context's own stream" to the C ABI
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     count = ctypes.c_uint64(0)
 
