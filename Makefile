@@ -6,7 +6,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
 PKG := paper_0909_2000_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/libalignplot_b200.so
-OBJS := build/ap_capi.o build/ap_inst_l8.o build/ap_inst_l16.o build/ap_inst_l32.o
+OBJS := build/ap_capi.o build/ap_inst_l8.o build/ap_inst_l16.o build/ap_inst_l32.o build/ap_inst_r2.o
 HDRS := $(CSRC)/ap_kernels.cuh $(CSRC)/ap_aux_kernels.cuh include/alignplot_b200.h
 
 all: $(LIB) oracle

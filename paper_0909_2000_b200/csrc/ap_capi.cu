@@ -78,6 +78,7 @@ uint32_t next_pow2(uint32_t v) {
 
 struct Shape {
   int L = 0, R = 0, K = 2;
+  bool r2 = false;   // r = 2 specialised kernel (comb2_kernel); R = 2*RR then
   bool xm = false;   // masks computed in registers (no table)
   uint32_t ring = 0;
   size_t smem = 0;
@@ -131,6 +132,53 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
         out->smem = smem;
         out->warps_per_sm = warps;
       }
+    }
+  }
+  return best < 1e29;
+}
+
+// r = 2 specialised shapes (L, RR real rows per lane, K bands): usable when
+// RR divides w and w/RR <= L (idle trailing lanes are padding).
+struct Shape2Def { int L, RR, K; };
+constexpr Shape2Def kShapes2[] = {
+    {4, 25, 5}, {8, 8, 2}, {8, 8, 4}, {16, 4, 2}, {16, 8, 4}, {32, 8, 4},
+    {8, 16, 4}, {16, 16, 4}, {32, 16, 4}, {32, 4, 2},
+};
+
+bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
+  if (std::getenv("AP_NO_R2")) return false;
+  const uint32_t W = 2 * w;
+  const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
+  double best = 1e30;
+  for (const Shape2Def& d : kShapes2) {
+    if (w % d.RR || w / d.RR > uint32_t(d.L)) continue;
+    KernelFn fn = apk::pick_r2(d.L, d.RR, d.K, dense);
+    if (!fn) continue;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    const int bw = apk::r2_band_words(d.RR / d.K);
+    const size_t smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(d.L, d.K * bw, sigma_y, ring, 2 * apk::kChunk);
+    if (smem > kSmemPerSm - 1024) continue;
+    const int by_regs = 65536 / (std::max(fa.numRegs, 1) * 32 * apk::kWarpsPerCta);
+    const int by_smem = int(kSmemPerSm / (smem + 1024));
+    const int ctas = std::min({by_regs, by_smem, 16});
+    if (ctas < 1) continue;
+    const int warps = ctas * apk::kWarpsPerCta;
+    double cost = double(d.L) * (6.0 * d.RR + 16.0) + 50.0;
+    if (warps < 16) cost *= 16.0 / warps;
+    if (cost < best) {
+      best = cost;
+      out->L = d.L;
+      out->R = 2 * d.RR;
+      out->K = d.K;
+      out->xm = false;
+      out->r2 = true;
+      out->ring = ring;
+      out->smem = smem;
+      out->warps_per_sm = warps;
     }
   }
   return best < 1e29;
@@ -271,23 +319,26 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const uint32_t sigma = sigma_y + (r == 2 ? 1 : 0);
 
   Shape sh;
-  if (!choose_shape(W, sigma, dense, &sh))
+  const bool spec = r == 2 && choose_shape2(w, sigma_y, dense, &sh);
+  if (!spec && !choose_shape(W, sigma, dense, &sh))
     return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                 sigma, W);
 
-  // code streams
+  // code streams: the specialised r = 2 kernel reads raw y codes (the $ columns
+  // are implicit); the generic kernel reads the $-interleaved stream
   if ((rc = grow(&c->d_xcode, &c->cap_xcode, mx))) return rc;
-  const size_t ytot = N + 256;
+  const size_t ylen = spec ? n : N;
+  const size_t ytot = ylen + 256;
   if ((rc = grow(&c->d_ycode, &c->cap_ycode, ytot))) return rc;
   apk::xcode_kernel<<<std::min<size_t>((mx + 255) / 256, 4096), 256, 0, st>>>(d_x, mx, c->d_map,
                                                                                c->d_xcode);
   CK(cudaGetLastError());
   apk::ycode_kernel<<<std::min<size_t>((ytot + 255) / 256, 4096), 256, 0, st>>>(
-      d_y, n, r, sent, c->d_map, c->d_ycode, ytot);
+      d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot);
   CK(cudaGetLastError());
   c->last_launches += 3;
 
-  KernelFn fn = pick_kernel(sh.L, sh.R, sh.K, dense, sh.xm);
+  KernelFn fn = spec ? apk::pick_r2(sh.L, sh.R / 2, sh.K, dense) : pick_kernel(sh.L, sh.R, sh.K, dense, sh.xm);
   if (!fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", sh.L, sh.R);
   CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem)));
@@ -310,7 +361,10 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t min_seg = std::max<size_t>(4 * W, 256);
   nseg = std::min(nseg, std::max<size_t>(1, out_cols_eff / min_seg));
   size_t S = (out_cols_eff + nseg - 1) / nseg;
-  S = (S + 31) & ~size_t(31);   // segment starts 32-aligned: 16-B vector loads of the code stream
+  // segment starts aligned for 16-B vector loads of the code stream (raw codes
+  // for the r = 2 kernel: blown starts multiple of 64)
+  const size_t salign = spec ? 64 : 32;
+  S = (S + salign - 1) / salign * salign;
   nseg = (out_cols_eff + S - 1) / S;
 
   apk::CombParams p{};
@@ -322,7 +376,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.r = r;
   p.W = W;
   p.N = uint32_t(N);
-  p.sigma = sh.xm ? 0 : sigma;
+  p.sigma = spec ? sigma_y : (sh.xm ? 0 : sigma);
   p.sent_code = sent;
   p.S = uint32_t(S);
   p.nseg = uint32_t(nseg);

@@ -78,6 +78,8 @@ using KernelFn = void (*)(CombParams);
 KernelFn pick_l8(int r, int k, bool dense, bool xm);
 KernelFn pick_l16(int r, int k, bool dense, bool xm);
 KernelFn pick_l32(int r, int k, bool dense, bool xm);
+// The r = 2 specialised kernels (ap_inst_r2.cu): RR real rows per lane.
+KernelFn pick_r2(int l, int rr, int k, bool dense);
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -94,13 +96,150 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t sel) {
   return d;
 }
 
-// Shared memory bytes per warp for a (L, R) instantiation.
-__host__ __device__ inline size_t comb_smem_per_warp(int L, int R, uint32_t sigma, uint32_t ring) {
+// Shared memory bytes per warp: mismatch table (table_words 32-bit words per
+// lane per code), the bottom-key ring (nb entries per chunk, padded by one word
+// per group so the bottom lanes of different groups hit different banks) and
+// the ok-flag rings.
+__host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uint32_t sigma, uint32_t ring,
+                                                     int nb = kChunk) {
   const int G = 32 / L;
-  const size_t bytes = size_t(128) * sigma * R   // mismatch table (sigma = 0 when masks are computed)
-       + size_t(G) * (kChunk + 1) * 4            // bottom-key ring per group (padded: no bank conflicts)
-       + size_t(G) * 2 * ring;                   // ok flags per group (strip A, strip B)
-  return (bytes + 15) & ~size_t(15);             // keep every warp's table 16-B aligned
+  const size_t bytes = size_t(4) * 32 * sigma * table_words   // mismatch table (sigma = 0: computed masks)
+       + size_t(G) * (nb + 1) * 4                              // bottom-key ring per group
+       + size_t(G) * 2 * ring;                                 // ok flags per group (strip A, strip B)
+  return (bytes + 15) & ~size_t(15);                           // keep every warp's table 16-B aligned
+}
+
+// Window extraction for the NB bottom columns [E0, E0 + NB) held in this
+// group's ring (one per step and blown column).  Lane j owns the CPL = NB/L
+// consecutive columns E0 + j*CPL + c.  Per column e with bottom key k the
+// seaweed is countable iff its span e - start < W (lane_kernel.cpp:79-87 keeps
+// exactly those spans); its start then gets an ok flag, and
+//   count(K+1) = count(K) + [column K+W countable] - ok[K]
+// (the heap of seaweed_scalar.cpp:80-97 replaced by a difference recurrence,
+// DESIGN.md §4), evaluated as a segmented scan over the group.  LLCS(K) =
+// W - count(K) is reported for K = 0 mod r and converted to half-units
+// (runner.cpp:31-35); dense mode stores it, threshold mode stages the hits
+// with their row-major rank (scoring.cpp:30-39).
+template <int L, int NB, bool DENSE>
+__device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_t* ringB, uint8_t* okA,
+                                              uint8_t* okB, uint32_t j, uint32_t g, uint32_t lane,
+                                              int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
+                                              uint32_t rA, uint32_t rB, bool hasA, bool hasB,
+                                              uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
+  const uint32_t rmask = p.ring - 1;
+  const uint32_t rshift = p.r - 1;
+  constexpr int CPL = NB / L;
+  const int32_t eb = E0 + int32_t(j) * CPL;
+  uint32_t cmask = 0;   // bit 2c: strip A countable, bit 2c+1: strip B
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int32_t e = eb + c;
+    const bool valid = e >= 0 && e < int32_t(nseg_cols);
+    const uint32_t k = ringB[j * CPL + c];
+    const int32_t thr = e - kbase - int32_t(p.W);
+    const int32_t kA = int32_t(k & 0xFFFFu), kB = int32_t(k >> 16);
+    const bool cA = valid && kA > thr;
+    const bool cB = valid && kB > thr;
+    if (cA) okA[uint32_t(kA + kbase) & rmask] = 1;
+    if (cB) okB[uint32_t(kB + kbase) & rmask] = 1;
+    cmask |= (uint32_t(cA) | (uint32_t(cB) << 1)) << (2 * c);
+  }
+  __syncwarp();
+  uint32_t dl[CPL];
+  uint32_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int32_t e = eb + c;
+    const bool valid = e >= 0 && e < int32_t(nseg_cols);
+    uint32_t oA = 0, oB = 0;
+    if (valid) {
+      const uint32_t slot = uint32_t(e - int32_t(p.W)) & rmask;
+      oA = okA[slot];
+      oB = okB[slot];
+      okA[slot] = 0;
+      okB[slot] = 0;
+    }
+    const uint32_t cA = (cmask >> (2 * c)) & 1u, cB = (cmask >> (2 * c + 1)) & 1u;
+    acc += (cA + 1u - oA) | ((cB + 1u - oB) << 16);   // biased by +1 per half
+    dl[c] = acc;
+  }
+  // exclusive scan of the lane totals across the group
+  uint32_t incl = acc;
+#pragma unroll
+  for (int off = 1; off < L; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off, L);
+    if (j >= uint32_t(off)) incl += v;
+  }
+  const uint32_t excl = incl - acc;
+  const uint32_t bias0 = j * CPL * 0x00010001u;
+  uint32_t hmA = 0, hmB = 0;      // threshold hits of this lane's columns (bit c)
+  uint32_t hv[DENSE ? 1 : CPL];   // packed half-unit scores hA | hB << 16
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int32_t e = eb + c;
+    const bool valid = e >= 0 && e < int32_t(nseg_cols);
+    const uint32_t cnt = run + excl + dl[c] - bias0 - uint32_t(c + 1) * 0x00010001u;
+    const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
+    const bool out_ok = valid && kp >= 0 && kp < int32_t(p.S) && !(uint32_t(kp) & rshift);
+    const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
+    const int32_t llA = int32_t(p.W) - int32_t(cnt & 0xFFFFu);
+    const int32_t llB = int32_t(p.W) - int32_t(cnt >> 16);
+    const int32_t hA = 2 * llA - (rshift ? 2 * int32_t(p.w) : 0);
+    const int32_t hB = 2 * llB - (rshift ? 2 * int32_t(p.w) : 0);
+    if constexpr (DENSE) {
+      if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
+      if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
+    } else {
+      hmA |= uint32_t(out_ok && hasA && hA >= p.t_half) << c;
+      hmB |= uint32_t(out_ok && hasB && hB >= p.t_half) << c;
+      hv[c] = uint32_t(hA) | (uint32_t(hB) << 16);
+    }
+  }
+  if constexpr (!DENSE) {
+    // Row-major ranks: a hit's rank in its (row, segment) = the row's earlier
+    // hits (previous chunks, lower lanes of this chunk, lower columns of this lane).
+    if (__any_sync(0xFFFFFFFFu, hmA | hmB)) {
+      const uint32_t nA = __popc(hmA), nB = __popc(hmB);
+      const uint32_t pk = nA | (nB << 16);
+      uint32_t gi = pk;
+#pragma unroll
+      for (int off = 1; off < L; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, gi, off, L);
+        if (j >= uint32_t(off)) gi += v;
+      }
+      const uint32_t gex = gi - pk;
+      const uint32_t gtot = __shfl_sync(0xFFFFFFFFu, gi, L - 1, L);
+      uint32_t wi = nA + nB;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, off);
+        if (lane >= uint32_t(off)) wi += v;
+      }
+      const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, wi, 31);
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(p.cursor, (unsigned long long)wtot);
+      pos = __shfl_sync(0xFFFFFFFFu, pos, 0) + (wi - nA - nB);
+      uint32_t rkA = hitsA + (gex & 0xFFFFu), rkB = hitsB + (gex >> 16);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const uint32_t gcol = (c0 + uint32_t(eb + c - int32_t(p.W) + 1)) >> rshift;
+        if ((hmA >> c) & 1u) {
+          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hv[c] & 0xFFFFu, rkA);
+          ++pos;
+          ++rkA;
+        }
+        if ((hmB >> c) & 1u) {
+          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hv[c] >> 16, rkB);
+          ++pos;
+          ++rkB;
+        }
+      }
+      hitsA += gtot & 0xFFFFu;
+      hitsB += gtot >> 16;
+    }
+  }
+  run = __shfl_sync(0xFFFFFFFFu, run + incl - (j + 1) * CPL * 0x00010001u, L - 1, L);
+  __syncwarp();
 }
 
 // Comb kernel (K2): fused $-interleave, seaweed combing, window extraction
@@ -308,123 +447,9 @@ comb_kernel(const CombParams p) {
       ych2 = nxb;
       __syncwarp();
 
-      // ---- window extraction for bottom columns [E0, E0 + 32); lane j owns the
-      //   CPL consecutive columns E0 + j*CPL + c.  Per column e with bottom key k:
-      //   countable iff span < W; then the seaweed's start st gets an ok flag, and
-      //   count(K+1) = count(K) + [e = K+W countable] - ok[K]   (K = e - W).
-      constexpr int CPL = kChunk / L;
-      const int32_t E0 = int32_t(ch * kChunk) - (VB - 1);
-      const int32_t eb = E0 + int32_t(j) * CPL;
-      uint32_t cmask = 0;   // bit 2c: strip A countable, bit 2c+1: strip B
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int32_t e = eb + c;
-        const bool valid = e >= 0 && e < int32_t(nseg_cols);
-        const uint32_t k = ringB[j * CPL + c];
-        const int32_t thr = e - kbase - int32_t(p.W);
-        const int32_t kA = int32_t(k & 0xFFFFu), kB = int32_t(k >> 16);
-        const bool cA = valid && kA > thr;
-        const bool cB = valid && kB > thr;
-        if (cA) okA[uint32_t(kA + kbase) & rmask] = 1;
-        if (cB) okB[uint32_t(kB + kbase) & rmask] = 1;
-        cmask |= (uint32_t(cA) | (uint32_t(cB) << 1)) << (2 * c);
-      }
-      __syncwarp();
-      uint32_t dl[CPL];
-      uint32_t acc = 0;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int32_t e = eb + c;
-        const bool valid = e >= 0 && e < int32_t(nseg_cols);
-        uint32_t oA = 0, oB = 0;
-        if (valid) {
-          const uint32_t slot = uint32_t(e - int32_t(p.W)) & rmask;
-          oA = okA[slot];
-          oB = okB[slot];
-          okA[slot] = 0;
-          okB[slot] = 0;
-        }
-        const uint32_t cA = (cmask >> (2 * c)) & 1u, cB = (cmask >> (2 * c + 1)) & 1u;
-        acc += (cA + 1u - oA) | ((cB + 1u - oB) << 16);   // biased by +1 per half
-        dl[c] = acc;
-      }
-      // exclusive scan of the lane totals across the group
-      uint32_t incl = acc;
-#pragma unroll
-      for (int off = 1; off < L; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off, L);
-        if (j >= uint32_t(off)) incl += v;
-      }
-      const uint32_t excl = incl - acc;
-      const uint32_t bias0 = j * CPL * 0x00010001u;
-      uint32_t hmA = 0, hmB = 0;      // threshold hits of this lane's columns (bit c)
-      uint32_t hv[DENSE ? 1 : CPL];   // packed half-unit scores hA | hB << 16
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int32_t e = eb + c;
-        const bool valid = e >= 0 && e < int32_t(nseg_cols);
-        const uint32_t cnt = run + excl + dl[c] - bias0 - uint32_t(c + 1) * 0x00010001u;
-        const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
-        const bool out_ok = valid && kp >= 0 && kp < int32_t(p.S) && !(uint32_t(kp) & rshift);
-        const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
-        const int32_t llA = int32_t(p.W) - int32_t(cnt & 0xFFFFu);
-        const int32_t llB = int32_t(p.W) - int32_t(cnt >> 16);
-        const int32_t hA = 2 * llA - (rshift ? 2 * int32_t(p.w) : 0);
-        const int32_t hB = 2 * llB - (rshift ? 2 * int32_t(p.w) : 0);
-        if constexpr (DENSE) {
-          if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
-          if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
-        } else {
-          hmA |= uint32_t(out_ok && hasA && hA >= p.t_half) << c;
-          hmB |= uint32_t(out_ok && hasB && hB >= p.t_half) << c;
-          hv[c] = uint32_t(hA) | (uint32_t(hB) << 16);
-        }
-      }
-      if constexpr (!DENSE) {
-        // Row-major ranks: a hit's rank in its (row, segment) = the row's earlier
-        // hits (previous chunks, lower lanes of this chunk, lower columns of this lane).
-        if (__any_sync(0xFFFFFFFFu, hmA | hmB)) {
-          const uint32_t nA = __popc(hmA), nB = __popc(hmB);
-          const uint32_t pk = nA | (nB << 16);
-          uint32_t gi = pk;
-#pragma unroll
-          for (int off = 1; off < L; off <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, gi, off, L);
-            if (j >= uint32_t(off)) gi += v;
-          }
-          const uint32_t gex = gi - pk;
-          const uint32_t gtot = __shfl_sync(0xFFFFFFFFu, gi, L - 1, L);
-          uint32_t wi = nA + nB;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, off);
-            if (lane >= uint32_t(off)) wi += v;
-          }
-          const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, wi, 31);
-          unsigned long long pos = 0;
-          if (lane == 0) pos = atomicAdd(p.cursor, (unsigned long long)wtot);
-          pos = __shfl_sync(0xFFFFFFFFu, pos, 0) + (wi - nA - nB);
-          uint32_t rkA = hitsA + (gex & 0xFFFFu), rkB = hitsB + (gex >> 16);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const uint32_t gcol = (c0 + uint32_t(eb + c - int32_t(p.W) + 1)) >> rshift;
-            if ((hmA >> c) & 1u) {
-              if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hv[c] & 0xFFFFu, rkA);
-              ++pos;
-              ++rkA;
-            }
-            if ((hmB >> c) & 1u) {
-              if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hv[c] >> 16, rkB);
-              ++pos;
-              ++rkB;
-            }
-          }
-          hitsA += gtot & 0xFFFFu;
-          hitsB += gtot >> 16;
-        }
-      }
-      run = __shfl_sync(0xFFFFFFFFu, run + incl - (j + 1) * CPL * 0x00010001u, L - 1, L);
-      __syncwarp();
+      extract_chunk<L, kChunk, DENSE>(p, ringB, okA, okB, j, g, lane,
+                                      int32_t(ch * kChunk) - (VB - 1), nseg_cols, kbase, c0, rA, rB,
+                                      hasA, hasB, run, hitsA, hitsB);
 
       // ---- key rebase (saturating at 0): fresh keys stay below 0x7BFF (fp16-finite)
       if (uint32_t(int32_t((ch + 2) * kChunk) - kbase) >= kRebaseAt) {
@@ -433,6 +458,228 @@ comb_kernel(const CombParams p) {
         for (int rho = 0; rho < R; ++rho) V[rho] = __vmaxu2(V[rho], by) - by;
 #pragma unroll
         for (int b = 0; b < K; ++b) tb[b] = __vmaxu2(tb[b], by) - by;
+        fresh -= by;
+        kbase += int32_t(kRebaseBy);
+      }
+    }
+    if constexpr (!DENSE) {
+      if (j == 0) {
+        if (hasA) p.seg_counts[size_t(rA) * p.nseg + seg] = hitsA;
+        if (hasB) p.seg_counts[size_t(rB) * p.nseg + seg] = hitsB;
+      }
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Alignment-score kernel (r = 2) specialised on the $-interleave
+// (scoring.cpp:5-17).  In the blown strip x'[2i] = y'[2k] = $ and windows start
+// at even offsets, so every cell's match status is static except real x real:
+//   ($ row, $ col)    always match   -> the two seaweeds swap: zero instructions
+//   ($ row, real col) never match    -> d = max(V,T), V' = min(V,T)
+//   (real row, $ col) never match    -> same
+//   (real row, real col)             -> table multiplier, HMUL2 + max + xor
+// (SURVEY.md §7 hard part 8).  A step is one raw column = the blown columns
+// 2c ($) and 2c+1 (real); two seaweeds per band move down per step.  The
+// table holds only real rows and real codes.  R = 2*RR blown rows per lane,
+// K bands of RRB = RR/K real rows; lanes j >= W/R (if any) are idle padding
+// whose output is never read (the bottom is lane W/R - 1's last band).
+template <int RRB>
+__device__ __forceinline__ void load_band_words(const uint32_t* base, uint32_t* m) {
+  constexpr int Q4 = RRB / 4, REM = RRB % 4;
+#pragma unroll
+  for (int q = 0; q < Q4; ++q) {
+    const uint4 v = reinterpret_cast<const uint4*>(base)[q];
+    m[4 * q] = v.x; m[4 * q + 1] = v.y; m[4 * q + 2] = v.z; m[4 * q + 3] = v.w;
+  }
+  if constexpr (REM >= 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(base + 4 * Q4);
+    m[4 * Q4] = v.x; m[4 * Q4 + 1] = v.y;
+  }
+  if constexpr (REM == 1 || REM == 3) m[RRB - 1] = base[RRB - 1];
+}
+
+// Words per (lane, band, code) in the r = 2 table: RRB padded to an aligned load group.
+__host__ __device__ constexpr int r2_band_words(int rrb) { return rrb <= 2 ? rrb : (rrb + 3) / 4 * 4; }
+
+template <int L, int RR, int K, bool DENSE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= 8 ? 4 : (RR <= 16 ? 3 : 2))
+comb2_kernel(const CombParams p) {
+  static_assert(32 % L == 0 && RR % K == 0, "bad shape");
+  constexpr int G = 32 / L;
+  constexpr int R = 2 * RR;
+  constexpr int RRB = RR / K;
+  constexpr int BW = r2_band_words(RRB);
+  constexpr int NB = 2 * kChunk;   // blown bottom columns per chunk
+  extern __shared__ __align__(16) unsigned char smem[];
+
+  const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t g = lane / L;
+  const uint32_t j = lane % L;
+  const size_t per_warp = comb_smem_per_warp(L, K * BW, p.sigma, p.ring, NB);
+  unsigned char* wbase = smem + warp * per_warp;
+  uint32_t* tbl = reinterpret_cast<uint32_t*>(wbase);                  // [G][sigma][K][L][BW]
+  const size_t tbl_bytes = size_t(4) * 32 * p.sigma * K * BW;
+  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * (NB + 1);
+  uint8_t* okA = wbase + tbl_bytes + G * (NB + 1) * 4 + size_t(g) * 2 * p.ring;
+  uint8_t* okB = okA + p.ring;
+
+  const uint32_t lanes_real = p.W / R;          // host guarantees W % R == 0, lanes_real <= L
+  const uint32_t VB = lanes_real * K;           // virtual bands down to the strip bottom
+  const uint32_t npairs = (p.rows + 1) / 2;
+  const uint32_t ngroups = (npairs + G - 1) / G;
+  const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
+  const uint64_t wstride = uint64_t(gridDim.x) * kWarpsPerCta;
+
+  for (uint64_t task = uint64_t(blockIdx.x) * kWarpsPerCta + warp; task < ntasks; task += wstride) {
+    const uint32_t pg = uint32_t(task / p.nseg);
+    const uint32_t seg = uint32_t(task % p.nseg);
+    const uint32_t pair = pg * G + g;
+    const uint32_t rA = 2 * pair, rB = 2 * pair + 1;
+    const bool hasA = rA < p.rows, hasB = rB < p.rows;
+    const uint32_t c0 = seg * p.S;                         // blown, multiple of 64
+    const uint32_t c0r = c0 >> 1;                          // raw, multiple of 32
+    const uint32_t nseg_cols = min(p.S + p.W - 1, p.N - c0);
+    const uint32_t nraw = (nseg_cols + 1) >> 1;
+    const uint32_t nsteps = nraw + VB - 1;
+    const uint32_t nch = (nsteps + kChunk - 1) / kChunk;
+
+    // ---- real-row multiplier table (real rows only, real codes only)
+    __syncwarp();
+    {
+      uint32_t xa[RR], xb[RR];
+#pragma unroll
+      for (int i = 0; i < RR; ++i) {
+        const uint32_t xi = j * RR + i;            // raw offset in the x-window
+        uint32_t ca = 0x1FFu, cb = 0x1FFu;
+        if (xi < p.w) {
+          if (hasA) ca = p.xcode[size_t(rA) * p.h + xi];
+          if (hasB) cb = p.xcode[size_t(rB) * p.h + xi];
+          if (ca == 0xFFu) ca = 0x1FFu;
+          if (cb == 0xFFu) cb = 0x1FFu;
+        }
+        xa[i] = ca;
+        xb[i] = cb;
+      }
+      for (uint32_t a = 0; a < p.sigma; ++a) {
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          uint32_t* dst = tbl + ((((size_t(g) * p.sigma + a) * K + b) * L) + j) * BW;
+#pragma unroll
+          for (int i = 0; i < RRB; ++i) {
+            const int rr = b * RRB + i;
+            dst[i] = (xa[rr] == a ? 0u : 0x00003C00u) | (xb[rr] == a ? 0u : 0x3C000000u);
+          }
+        }
+      }
+      for (uint32_t k = j; k < 2 * p.ring; k += L) okA[k] = 0;
+    }
+    __syncwarp();
+
+    const uint32_t* tl = tbl + ((size_t(g) * p.sigma * K) * L + j) * BW;
+    const size_t code_stride = size_t(K) * L * BW;   // words between consecutive codes
+    const uint32_t* yw = reinterpret_cast<const uint32_t*>(p.ycode + c0r);
+
+    uint32_t V[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) V[i] = 0u;
+    uint32_t tbD[K], tbR[K], cd[K];
+#pragma unroll
+    for (int b = 0; b < K; ++b) { tbD[b] = 0u; tbR[b] = 0u; cd[b] = 0u; }
+    int32_t kbase = -int32_t(p.W) - 1;
+    uint32_t fresh = uint32_t(-kbase) * 0x00010001u;   // key of blown column 2s
+    uint32_t run = 0u, hitsA = 0u, hitsB = 0u;
+
+    uint4 ych = __ldg(reinterpret_cast<const uint4*>(yw));
+    uint4 ych2 = __ldg(reinterpret_cast<const uint4*>(yw) + 1);
+    if (j == 0) cd[0] = ych.x & 0xFFu;
+
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+      const uint4 nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
+      const uint4 nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
+#pragma unroll 1
+      for (int sub = 0; sub < kChunk / 8; ++sub) {
+        const uint32_t w0 = sub == 0 ? ych.x : sub == 1 ? ych.z : sub == 2 ? ych2.x : ych2.z;
+        const uint32_t w1 = sub == 0 ? ych.y : sub == 1 ? ych.w : sub == 2 ? ych2.y : ych2.w;
+        const uint32_t w2 = sub == 0 ? ych.z : sub == 1 ? ych2.x : sub == 2 ? ych2.z : nxa.x;
+        uint32_t* ring_sub = ringB + sub * 16;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint32_t m[K][RRB];
+#pragma unroll
+          for (int b = 0; b < K; ++b) load_band_words<RRB>(tl + cd[b] * code_stride + size_t(b) * L * BW, m[b]);
+          uint32_t tinD[K], tinR[K];
+          {
+            const uint32_t shD = __shfl_up_sync(0xFFFFFFFFu, tbD[K - 1], 1, L);
+            const uint32_t shR = __shfl_up_sync(0xFFFFFFFFu, tbR[K - 1], 1, L);
+            tinD[0] = j == 0 ? fresh : shD;
+            tinR[0] = j == 0 ? fresh + 0x00010001u : shR;
+#pragma unroll
+            for (int b = 1; b < K; ++b) { tinD[b] = tbD[b - 1]; tinR[b] = tbR[b - 1]; }
+          }
+          fresh += 0x00020002u;
+#pragma unroll
+          for (int b = 0; b < K; ++b) {
+            uint32_t t = tinD[b];                       // blown column 2c: $
+#pragma unroll
+            for (int i = 0; i < RRB; ++i) {
+              uint32_t& vs = V[b * 2 * RRB + 2 * i];     // $ row: match -> swap
+              const uint32_t sw = vs;
+              vs = t;
+              t = sw;
+              uint32_t& vr = V[b * 2 * RRB + 2 * i + 1]; // real row: mismatch
+              const uint32_t d = __vmaxu2(vr, t);
+              vr = __vminu2(vr, t);
+              t = d;
+            }
+            tbD[b] = t;
+            t = tinR[b];                                // blown column 2c+1: real char
+#pragma unroll
+            for (int i = 0; i < RRB; ++i) {
+              uint32_t& vs = V[b * 2 * RRB + 2 * i];     // $ row: mismatch
+              const uint32_t d0 = __vmaxu2(vs, t);
+              vs = __vminu2(vs, t);
+              t = d0;
+              uint32_t& vr = V[b * 2 * RRB + 2 * i + 1]; // real x real: table
+              uint32_t tt;
+              asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(tt) : "r"(t), "r"(m[b][i]));
+              const uint32_t d1 = __vmaxu2(vr, tt);
+              vr = lop3_xor(vr, t, d1);
+              t = d1;
+            }
+            tbR[b] = t;
+          }
+          if (j == lanes_real - 1) {
+            ring_sub[2 * u] = tbD[K - 1];
+            ring_sub[2 * u + 1] = tbR[K - 1];
+          }
+          {
+            const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
+            const uint32_t ynew = (ww >> (8 * ((u + 1) & 3))) & 0xFFu;
+            const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, cd[K - 1], 1, L);
+#pragma unroll
+            for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
+            cd[0] = j == 0 ? ynew : sh;
+          }
+        }
+      }
+      ych = nxa;
+      ych2 = nxb;
+      __syncwarp();
+      extract_chunk<L, NB, DENSE>(p, ringB, okA, okB, j, g, lane,
+                                  2 * (int32_t(ch * kChunk) - int32_t(VB - 1)), nseg_cols, kbase, c0, rA,
+                                  rB, hasA, hasB, run, hitsA, hitsB);
+      if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= kRebaseAt) {
+        const uint32_t by = kRebaseBy * 0x00010001u;
+#pragma unroll
+        for (int i = 0; i < R; ++i) V[i] = __vmaxu2(V[i], by) - by;
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          tbD[b] = __vmaxu2(tbD[b], by) - by;
+          tbR[b] = __vmaxu2(tbR[b], by) - by;
+        }
         fresh -= by;
         kbase += int32_t(kRebaseBy);
       }
