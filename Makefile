@@ -28,3 +28,9 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# C++ drop-in test (reference test cases against alignplot_shim.hpp); runs on a GPU box.
+tests/cpp/test_shim: tests/cpp/test_shim.cpp $(CSRC)/alignplot_shim.hpp include/alignplot_b200.h $(LIB)
+	g++ -std=c++20 -O2 -o $@ $< -L$(PKG) -lalignplot_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+all: tests/cpp/test_shim

@@ -132,3 +132,15 @@ def test_window_equals_input():
     assert g.shape == (1, 1) and g[0, 0] == 10
     g = gpu_grid(x, x, 5, 1, 2)
     assert g[0, 0] == 10
+
+
+def test_cpp_shim_reference_cases():
+    """The reference's own test cases, written against the C++ drop-in header, run on the GPU."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "test_shim")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", root, "tests/cpp/test_shim"], check=True)
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
