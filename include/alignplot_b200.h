@@ -82,6 +82,13 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
                       uint64_t* count, uint32_t* rows, uint32_t* cols, uint16_t* halves,
                       size_t cap);
 
+/* Dense 8-bit PGM raster of rows [row_begin, row_end), the pixels of
+ * write_pgm (io.cpp:136-153) quantised inside the comb kernel:
+ * pixel = (255 * clamp(half, 0, 2w) + w) / (2w), and, when has_threshold,
+ * 0 for cells below threshold_half.  Header formatting stays on the host. */
+int ap_plot_pgm(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                uint8_t* pixels);
+
 /* Message for the calling thread's last non-OK status. */
 const char* ap_last_error(void);
 
@@ -100,6 +107,10 @@ int ap_ctx_destroy(ap_ctx* ctx);
  * Sentinel bytes are not checked (the host API checks them). */
 int ap_ctx_plot_dense_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y,
                              size_t n, const ap_config* cfg, uint16_t* d_out, void* stream);
+
+/* As ap_plot_pgm on device pointers (enqueue only). */
+int ap_ctx_plot_pgm_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                           const ap_config* cfg, uint8_t* d_pixels, void* stream);
 
 /* Thresholded plot into device arrays of capacity cap; *count (host) gets the
  * total.  Synchronises ctx's stream. */

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <optional>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -298,6 +299,66 @@ inline std::vector<PlotCell> compute_plot_threshold(const Sequence& x, const Seq
   std::vector<PlotCell> out(count);
   for (std::size_t k = 0; k < count; ++k) out[k] = {rr[k], cc[k], hh[k]};
   return out;
+}
+
+// ---- writers (io.cpp:102-153), byte-identical ------------------------------
+inline std::string half_to_decimal(half_score_t half) {
+  const bool neg = half < 0;
+  const long long a = neg ? -static_cast<long long>(half) : half;
+  std::string out = neg ? "-" : "";
+  out += std::to_string(a / 2);
+  out += (a % 2) ? ".5" : ".0";
+  return out;
+}
+
+inline void write_tsv(std::ostream& out, const PlotGrid& grid, std::optional<half_score_t> threshold_half,
+                      bool dense) {
+  out << "# x_offset y_offset score\n";
+  for (std::size_t r = 0; r < grid.rows; ++r)
+    for (std::size_t c = 0; c < grid.cols; ++c) {
+      const half_score_t v = grid.at(r, c);
+      if (!dense && threshold_half && v < *threshold_half) continue;
+      out << grid.x_offset(r) << '\t' << grid.y_offset(c) << '\t' << half_to_decimal(v) << '\n';
+    }
+  if (!out) throw std::runtime_error("write failure on TSV sink");
+}
+
+inline void write_dots(std::ostream& out, const PlotGrid& grid, std::optional<half_score_t> threshold_half) {
+  for (std::size_t r = 0; r < grid.rows; ++r)
+    for (std::size_t c = 0; c < grid.cols; ++c) {
+      if (threshold_half && grid.at(r, c) < *threshold_half) continue;
+      out << grid.x_offset(r) << ' ' << grid.y_offset(c) << '\n';
+    }
+  if (!out) throw std::runtime_error("write failure on dot sink");
+}
+
+inline void write_pgm(std::ostream& out, const PlotGrid& grid, std::optional<half_score_t> threshold_half) {
+  out << "P5\n" << grid.cols << ' ' << grid.rows << "\n255\n";
+  const long long full = 2 * static_cast<long long>(grid.window_w);
+  std::vector<unsigned char> row(grid.cols);
+  for (std::size_t r = 0; r < grid.rows; ++r) {
+    for (std::size_t c = 0; c < grid.cols; ++c) {
+      half_score_t v = grid.at(r, c);
+      if (threshold_half && v < *threshold_half) v = 0;
+      const long long h = std::clamp<long long>(v, 0, full);
+      row[c] = static_cast<unsigned char>((255 * h + full / 2) / full);
+    }
+    out.write(reinterpret_cast<const char*>(row.data()), static_cast<std::streamsize>(row.size()));
+  }
+  if (!out) throw std::runtime_error("write failure on PGM sink");
+}
+
+// The PGM of compute_plot(x, y, cfg) without a dense grid on the host: pixels
+// are quantised inside the comb kernel (ap_plot_pgm), cfg.threshold_half cuts.
+inline void write_pgm_gpu(std::ostream& out, const Sequence& x, const Sequence& y, const PlotConfig& cfg) {
+  cfg.validate(x.size(), y.size());
+  const auto [rows, cols] = window_grid_dims(x.size(), y.size(), cfg.window_w, cfg.step_h);
+  std::vector<unsigned char> pix(rows * cols);
+  const ap_config c = cfg.to_c();
+  detail::check(ap_plot_pgm(x.data.data(), x.size(), y.data.data(), y.size(), &c, pix.data()));
+  out << "P5\n" << cols << ' ' << rows << "\n255\n";
+  out.write(reinterpret_cast<const char*>(pix.data()), static_cast<std::streamsize>(pix.size()));
+  if (!out) throw std::runtime_error("write failure on PGM sink");
 }
 
 }  // namespace alignplot

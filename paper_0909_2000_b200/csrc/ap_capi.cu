@@ -293,10 +293,12 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
 
 // Enqueue the whole pipeline for local rows [0, nrows) whose x windows start
 // at d_x (already offset to the first row).  dense: writes d_out.
+// out_kind (dense only): 0 = uint16 half-units into d_out, 1 = uint8 PGM pixels
+// (io.cpp:136-153 fused; cfg->has_threshold renders cells below it black).
 int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
                const ap_config* cfg, size_t nrows, size_t row_global0, bool dense,
-               uint16_t* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
-               uint32_t* d_orow, uint32_t* d_ocol, uint16_t* d_ohalf, size_t cap) {
+               void* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
+               uint32_t* d_orow, uint32_t* d_ocol, uint16_t* d_ohalf, size_t cap, int out_kind = 0) {
   const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
   const uint32_t W = w * r;
   const size_t N = n * r;
@@ -383,7 +385,11 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.ring = sh.ring;
   p.cols = uint32_t(cols);
   p.row_global0 = uint32_t(row_global0);
-  p.out = d_out;
+  p.out = static_cast<uint16_t*>(d_out);
+  p.out8 = static_cast<uint8_t*>(d_out);
+  p.out_kind = uint32_t(out_kind);
+  p.pgm_threshold = cfg->threshold_half;
+  p.has_pgm_threshold = cfg->has_threshold ? 1u : 0u;
 
   const size_t ntasks = ngroups * nseg;
   const size_t ctas_needed = (ntasks + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta;
@@ -560,6 +566,22 @@ int ap_ctx_plot_dense_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint
                     nullptr, nullptr, nullptr, nullptr, 0);
 }
 
+int ap_ctx_plot_pgm_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                           const ap_config* cfg, uint8_t* d_pixels, void* stream) {
+  if (!c || !d_x || !d_y || !d_pixels) return fail(AP_INVALID, "null argument");
+  int rc = check_cfg(m, n, cfg);
+  if (rc) return rc;
+  size_t rows, cols, rb, re;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
+  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DevGuard dg(c->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const size_t off = rb * cfg->step_h;
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_pixels, st, nullptr,
+                    nullptr, nullptr, nullptr, nullptr, 0, 1);
+}
+
 int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y,
                                  size_t n, const ap_config* cfg, uint64_t* count, uint32_t* d_rows,
                                  uint32_t* d_cols, uint16_t* d_halves, size_t cap, void* stream) {
@@ -590,8 +612,8 @@ bool has_sentinel(const uint8_t* p, size_t n) { return std::memchr(p, 0, n) != n
 
 // Shared host-API body: validates, shards rows over devices, runs, gathers.
 int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
-              bool dense, uint16_t* out_half, uint64_t* count, uint32_t* orow, uint32_t* ocol,
-              uint16_t* ohalf, size_t cap) {
+              bool dense, void* out_dense, uint64_t* count, uint32_t* orow, uint32_t* ocol,
+              uint16_t* ohalf, size_t cap, int out_kind = 0) {
   if (!x || !y || !cfg) return fail(AP_INVALID, "null argument");
   int rc = check_cfg(m, n, cfg);
   if (rc) return rc;
@@ -600,7 +622,8 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   size_t rows, cols, rb, re;
   ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
   if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
-  if (dense && !out_half && re > rb) return fail(AP_INVALID, "null output");
+  if (dense && !out_dense && re > rb) return fail(AP_INVALID, "null output");
+  const size_t out_elem = out_kind == 1 ? 1 : 2;
   const int ndev_avail = ap_device_count();
   if (ndev_avail <= 0) return fail(AP_NODEV, "no CUDA device available (the engine has no CPU fallback)");
   int ndev = cfg->n_devices <= 1 ? 1 : std::min(cfg->n_devices, ndev_avail);
@@ -644,10 +667,10 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
       if (dense) {
         if ((q = grow(&c->d_out, &c->cap_out, nrows * cols))) return q;
         if ((q = run_device(c, c->d_x, x1 - x0, c->d_y, n, cfg, nrows, s.r0, true, c->d_out, st,
-                            nullptr, nullptr, nullptr, nullptr, nullptr, 0)))
+                            nullptr, nullptr, nullptr, nullptr, nullptr, 0, out_kind)))
           return q;
-        CK(cudaMemcpyAsync(out_half + (s.r0 - rb) * cols, c->d_out, nrows * cols * sizeof(uint16_t),
-                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(static_cast<char*>(out_dense) + (s.r0 - rb) * cols * out_elem, c->d_out,
+                           nrows * cols * out_elem, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
       } else {
         // first pass sizes the list (counts are exact even if staging is short)
@@ -706,7 +729,17 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
 
 int ap_plot_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                   uint16_t* out_half) {
+  if (cfg && cfg->has_threshold) {
+    ap_config c = *cfg;   // the dense grid is never filtered (compute_plot, runner.cpp:78-131)
+    c.has_threshold = 0;
+    return host_plot(x, m, y, n, &c, true, out_half, nullptr, nullptr, nullptr, nullptr, 0);
+  }
   return host_plot(x, m, y, n, cfg, true, out_half, nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+int ap_plot_pgm(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                uint8_t* pixels) {
+  return host_plot(x, m, y, n, cfg, true, pixels, nullptr, nullptr, nullptr, nullptr, 0, 1);
 }
 
 int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,

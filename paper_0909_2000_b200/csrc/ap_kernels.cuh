@@ -63,7 +63,11 @@ struct CombParams {
   uint32_t cols;          // grid columns
   uint32_t row_global0;   // global grid row of local row 0
   // dense output
-  uint16_t* out;          // [rows][cols]
+  uint16_t* out;          // [rows][cols] half-units (out_kind 0)
+  uint8_t* out8;          // [rows][cols] PGM pixels (out_kind 1, io.cpp:136-153 fused)
+  uint32_t out_kind;      // 0 = uint16 half-units, 1 = uint8 PGM pixels
+  int32_t pgm_threshold;  // cells below it render 0 (when has_pgm_threshold)
+  uint32_t has_pgm_threshold;
   // thresholded output
   int32_t t_half;
   uint4* stage;                   // {row, col, half, rank} records
@@ -187,8 +191,19 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
     const int32_t hA = 2 * llA - (rshift ? 2 * int32_t(p.w) : 0);
     const int32_t hB = 2 * llB - (rshift ? 2 * int32_t(p.w) : 0);
     if constexpr (DENSE) {
-      if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
-      if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
+      if (p.out_kind == 0) {
+        if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
+        if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
+      } else {
+        // write_pgm (io.cpp:136-153): pixel = (255*clamp(h,0,2w) + w) / 2w, cut -> 0
+        const int32_t full = 2 * int32_t(p.w);
+        const bool cutA = p.has_pgm_threshold && hA < p.pgm_threshold;
+        const bool cutB = p.has_pgm_threshold && hB < p.pgm_threshold;
+        const int32_t qA = cutA ? 0 : (255 * min(max(hA, 0), full) + full / 2) / full;
+        const int32_t qB = cutB ? 0 : (255 * min(max(hB, 0), full) + full / 2) / full;
+        if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(qA);
+        if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(qB);
+      }
     } else {
       hmA |= uint32_t(out_ok && hasA && hA >= p.t_half) << c;
       hmB |= uint32_t(out_ok && hasB && hB >= p.t_half) << c;

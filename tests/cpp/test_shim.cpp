@@ -5,6 +5,7 @@
 // independent per-window DP (as tests/test_util.hpp's ref_llcs /
 // ref_align_score_half).  Exit status = number of failed checks.  Needs a GPU.
 #include <cstdio>
+#include <sstream>
 #include <random>
 #include <string>
 #include <vector>
@@ -172,6 +173,26 @@ int main() {
     CHECK(b.data == (std::vector<std::uint8_t>{0, 'a', 0, 'b', 0, 'a', 0, 'b'}));
     CHECK(unblow(b) == Sequence::from_text("s", "abab").data);
     CHECK(recover_score(4, 2, 2) == 4 && recover_score(2, 2, 2) == 0 && recover_score(2, 1, 2) == 1);
+  }
+  {  // test_io.cpp:155-252 writers, and the fused GPU PGM against the host writer
+    PlotGrid g(2, 2, 4, 5);
+    g.at(0, 0) = 4; g.at(0, 1) = 1; g.at(1, 0) = 3; g.at(1, 1) = 8;
+    std::ostringstream all;
+    write_tsv(all, g, std::nullopt, false);
+    CHECK(all.str() == "# x_offset y_offset score\n0\t0\t2.0\n0\t1\t0.5\n5\t0\t1.5\n5\t1\t4.0\n");
+    std::ostringstream dots;
+    write_dots(dots, g, half_score_t{3});
+    CHECK(dots.str() == "0 0\n5 0\n5 1\n");
+    std::mt19937 rng(560);
+    const Sequence x("x", random_codes(rng, 200, 4)), y("y", random_codes(rng, 260, 4));
+    for (unsigned r : {1u, 2u}) {
+      PlotConfig cfg;
+      cfg.window_w = 20; cfg.step_h = 3; cfg.blowup_r = r; cfg.threshold_half = 18;
+      std::ostringstream host, dev;
+      write_pgm(host, compute_plot(x, y, cfg), cfg.threshold_half);
+      write_pgm_gpu(dev, x, y, cfg);
+      CHECK(host.str() == dev.str());
+    }
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
   return failures;

@@ -144,3 +144,15 @@ def test_cpp_shim_reference_cases():
         subprocess.run(["make", "-C", root, "tests/cpp/test_shim"], check=True)
     res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+def test_pgm_fused_matches_host_quantisation():
+    from paper_0909_2000_b200 import writers as wr
+    rng = np.random.default_rng(31)
+    for w, h, r, t in ((30, 1, 1, None), (25, 2, 2, 20), (64, 1, 1, 100)):
+        x = rng.integers(1, 5, 400).astype(np.uint8)
+        y = np.concatenate([x[100:300], rng.integers(1, 5, 200)]).astype(np.uint8)
+        c = cfg(w, h, r, t)
+        rc, want = ol.plot_rows(x, y, w, h, r)
+        g = ap.PlotGrid(want.shape[0], want.shape[1], w, h, values=want.reshape(-1))
+        assert wr.plot_pgm(x, y, c) == wr.pgm_header(*want.shape) + wr.pgm_pixels(g, t).tobytes()
