@@ -191,7 +191,9 @@ struct ap_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream_copy = nullptr;   // D2H of finished row blocks (overlaps the comb kernel)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_blk[8] = {};
   std::mutex mu;
   // scratch (grown on demand)
   uint8_t *d_x = nullptr, *d_y = nullptr, *d_xcode = nullptr, *d_ycode = nullptr, *d_map = nullptr;
@@ -298,7 +300,8 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
 int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
                const ap_config* cfg, size_t nrows, size_t row_global0, bool dense,
                void* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
-               uint32_t* d_orow, uint32_t* d_ocol, uint16_t* d_ohalf, size_t cap, int out_kind = 0) {
+               uint32_t* d_orow, uint32_t* d_ocol, uint16_t* d_ohalf, size_t cap, int out_kind = 0,
+               void* host_out = nullptr) {
   const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
   const uint32_t W = w * r;
   const size_t N = n * r;
@@ -414,6 +417,42 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   }
 
   CK(cudaEventRecord(c->ev0, st));
+  if (dense && host_out) {
+    // Dense output to the host: launch the plot as row blocks of about one
+    // wave each and stream every finished block's D2H on the copy stream, so
+    // the PCIe transfer overlaps the comb kernel of the next block.
+    const size_t waves = (ntasks + total_warps - 1) / total_warps;
+    const size_t nblk = std::min<size_t>(std::max<size_t>(waves, 1), 8);
+    const size_t gpb = (ngroups + nblk - 1) / nblk;          // pair groups per block
+    const size_t elem = out_kind == 1 ? 1 : 2;
+    for (size_t k = 0; k < nblk; ++k) {
+      const size_t r0 = std::min(nrows, k * gpb * 2 * G), r1 = std::min(nrows, (k + 1) * gpb * 2 * G);
+      if (r0 >= r1) break;
+      apk::CombParams pk = p;
+      pk.xcode = c->d_xcode + r0 * h;
+      pk.rows = uint32_t(r1 - r0);
+      pk.row_global0 = uint32_t(row_global0 + r0);
+      pk.out = p.out + (out_kind == 1 ? 0 : r0 * cols);
+      pk.out8 = p.out8 + (out_kind == 1 ? r0 * cols : 0);
+      const size_t tk = ((r1 - r0 + 1) / 2 + G - 1) / G * nseg;
+      const size_t gk = std::min<size_t>((tk + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta, size_t(c->sms) * per_sm);
+      fn<<<dim3(unsigned(gk)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(pk);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(c->ev_blk[k], st));
+      c->last_launches += 1;
+    }
+    CK(cudaEventRecord(c->ev1, st));
+    for (size_t k = 0; k < nblk; ++k) {
+      const size_t r0 = std::min(nrows, k * gpb * 2 * G), r1 = std::min(nrows, (k + 1) * gpb * 2 * G);
+      if (r0 >= r1) break;
+      CK(cudaStreamWaitEvent(c->stream_copy, c->ev_blk[k], 0));
+      CK(cudaMemcpyAsync(static_cast<char*>(host_out) + r0 * cols * elem,
+                         static_cast<const char*>(d_out) + r0 * cols * elem, (r1 - r0) * cols * elem,
+                         cudaMemcpyDeviceToHost, c->stream_copy));
+    }
+    CK(cudaStreamSynchronize(c->stream_copy));
+    return AP_OK;
+  }
   fn<<<dim3(unsigned(grid)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev1, st));
@@ -503,6 +542,8 @@ int ap_ctx_create(int device, ap_ctx** out) {
   CK(cudaGetDeviceProperties(&prop, device));
   c->sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+  for (auto& e : c->ev_blk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
   CK(cudaMalloc(&c->d_small, 64));
@@ -530,9 +571,12 @@ int ap_ctx_destroy(ap_ctx* c) {
     if (p) cudaFree(p);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_cursor) cudaFreeHost(c->h_cursor);
+  cudaStreamSynchronize(c->stream_copy);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
+  for (auto& e : c->ev_blk) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->stream_copy);
   delete c;
   return AP_OK;
 }
@@ -667,10 +711,9 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
       if (dense) {
         if ((q = grow(&c->d_out, &c->cap_out, nrows * cols))) return q;
         if ((q = run_device(c, c->d_x, x1 - x0, c->d_y, n, cfg, nrows, s.r0, true, c->d_out, st,
-                            nullptr, nullptr, nullptr, nullptr, nullptr, 0, out_kind)))
+                            nullptr, nullptr, nullptr, nullptr, nullptr, 0, out_kind,
+                            static_cast<char*>(out_dense) + (s.r0 - rb) * cols * out_elem)))
           return q;
-        CK(cudaMemcpyAsync(static_cast<char*>(out_dense) + (s.r0 - rb) * cols * out_elem, c->d_out,
-                           nrows * cols * out_elem, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
       } else {
         // first pass sizes the list (counts are exact even if staging is short)
