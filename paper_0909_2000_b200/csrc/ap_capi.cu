@@ -143,12 +143,25 @@ struct Shape2Def { int L, RR, K; };
 constexpr Shape2Def kShapes2[] = {
     {4, 25, 5}, {8, 8, 2}, {8, 8, 4}, {16, 4, 2}, {16, 8, 4}, {32, 8, 4},
     {8, 16, 4}, {16, 16, 4}, {32, 16, 4}, {32, 4, 2},
+    {8, 20, 4}, {16, 10, 2}, {32, 5, 1}, {4, 25, 1}, {32, 4, 1}, {16, 4, 1},
 };
 
 bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
   if (std::getenv("AP_NO_R2")) return false;
   const uint32_t W = 2 * w;
   const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
+  // tuning override: AP_SHAPE2="L,RR,K"
+  if (const char* env = std::getenv("AP_SHAPE2")) {
+    int l = 0, rr = 0, k = 0;
+    if (std::sscanf(env, "%d,%d,%d", &l, &rr, &k) == 3 && apk::pick_r2(l, rr, k, dense) && rr > 0 &&
+        w % rr == 0 && w / rr <= uint32_t(l)) {
+      out->L = l; out->R = 2 * rr; out->K = k; out->xm = false; out->r2 = true; out->ring = ring;
+      out->smem = apk::kWarpsPerCta *
+                  apk::comb_smem_per_warp(l, k * apk::r2_band_words(rr / k), sigma_y, ring, 2 * apk::kChunk);
+      out->warps_per_sm = 0;
+      return out->smem <= kSmemPerSm - 1024;
+    }
+  }
   double best = 1e30;
   for (const Shape2Def& d : kShapes2) {
     if (w % d.RR || w / d.RR > uint32_t(d.L)) continue;

@@ -500,23 +500,28 @@ comb_kernel(const CombParams p) {
 // table holds only real rows and real codes.  R = 2*RR blown rows per lane,
 // K bands of RRB = RR/K real rows; lanes j >= W/R (if any) are idle padding
 // whose output is never read (the bottom is lane W/R - 1's last band).
+// r = 2 table layout: per (group, code, band, lane) index idx the band's RRB
+// real-row words are split into Q4 = RRB/4 quads in tblq[idx*Q4 + q] (LDS.128)
+// and REM = RRB%4 (0..2) words in tblr[idx*REM + k] (LDS.64 / LDS.32): no
+// padding, every load naturally aligned.
+__host__ __device__ constexpr int r2_band_words(int rrb) { return rrb; }
+
 template <int RRB>
-__device__ __forceinline__ void load_band_words(const uint32_t* base, uint32_t* m) {
+__device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t* tr, size_t idx, uint32_t* m) {
   constexpr int Q4 = RRB / 4, REM = RRB % 4;
+  static_assert(REM <= 2, "band real-row count must be 4q, 4q+1 or 4q+2");
 #pragma unroll
   for (int q = 0; q < Q4; ++q) {
-    const uint4 v = reinterpret_cast<const uint4*>(base)[q];
+    const uint4 v = tq[idx * Q4 + q];
     m[4 * q] = v.x; m[4 * q + 1] = v.y; m[4 * q + 2] = v.z; m[4 * q + 3] = v.w;
   }
-  if constexpr (REM >= 2) {
-    const uint2 v = *reinterpret_cast<const uint2*>(base + 4 * Q4);
+  if constexpr (REM == 2) {
+    const uint2 v = reinterpret_cast<const uint2*>(tr)[idx];
     m[4 * Q4] = v.x; m[4 * Q4 + 1] = v.y;
+  } else if constexpr (REM == 1) {
+    m[4 * Q4] = tr[idx];
   }
-  if constexpr (REM == 1 || REM == 3) m[RRB - 1] = base[RRB - 1];
 }
-
-// Words per (lane, band, code) in the r = 2 table: RRB padded to an aligned load group.
-__host__ __device__ constexpr int r2_band_words(int rrb) { return rrb <= 2 ? rrb : (rrb + 3) / 4 * 4; }
 
 template <int L, int RR, int K, bool DENSE>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= 8 ? 4 : (RR <= 16 ? 3 : 2))
@@ -526,6 +531,7 @@ comb2_kernel(const CombParams p) {
   constexpr int R = 2 * RR;
   constexpr int RRB = RR / K;
   constexpr int BW = r2_band_words(RRB);
+  constexpr int Q4 = RRB / 4, REM = RRB % 4;
   constexpr int NB = 2 * kChunk;   // blown bottom columns per chunk
   extern __shared__ __align__(16) unsigned char smem[];
 
@@ -535,7 +541,9 @@ comb2_kernel(const CombParams p) {
   const uint32_t j = lane % L;
   const size_t per_warp = comb_smem_per_warp(L, K * BW, p.sigma, p.ring, NB);
   unsigned char* wbase = smem + warp * per_warp;
-  uint32_t* tbl = reinterpret_cast<uint32_t*>(wbase);                  // [G][sigma][K][L][BW]
+  const size_t nidx = size_t(G) * p.sigma * K * L;                     // (group, code, band, lane)
+  uint4* tblq = reinterpret_cast<uint4*>(wbase);                       // [nidx][Q4]
+  uint32_t* tblr = reinterpret_cast<uint32_t*>(tblq + nidx * Q4);      // [nidx][REM]
   const size_t tbl_bytes = size_t(4) * 32 * p.sigma * K * BW;
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * (NB + 1);
   uint8_t* okA = wbase + tbl_bytes + G * (NB + 1) * 4 + size_t(g) * 2 * p.ring;
@@ -581,20 +589,25 @@ comb2_kernel(const CombParams p) {
       for (uint32_t a = 0; a < p.sigma; ++a) {
 #pragma unroll
         for (int b = 0; b < K; ++b) {
-          uint32_t* dst = tbl + ((((size_t(g) * p.sigma + a) * K + b) * L) + j) * BW;
+          const size_t idx = ((size_t(g) * p.sigma + a) * K + b) * L + j;
+          uint32_t wv[RRB];
 #pragma unroll
           for (int i = 0; i < RRB; ++i) {
             const int rr = b * RRB + i;
-            dst[i] = (xa[rr] == a ? 0u : 0x00003C00u) | (xb[rr] == a ? 0u : 0x3C000000u);
+            wv[i] = (xa[rr] == a ? 0u : 0x00003C00u) | (xb[rr] == a ? 0u : 0x3C000000u);
           }
+#pragma unroll
+          for (int q = 0; q < Q4; ++q)
+            tblq[idx * Q4 + q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+#pragma unroll
+          for (int k = 0; k < REM; ++k) tblr[idx * REM + k] = wv[4 * Q4 + k];
         }
       }
       for (uint32_t k = j; k < 2 * p.ring; k += L) okA[k] = 0;
     }
     __syncwarp();
 
-    const uint32_t* tl = tbl + ((size_t(g) * p.sigma * K) * L + j) * BW;
-    const size_t code_stride = size_t(K) * L * BW;   // words between consecutive codes
+    const size_t idx0 = (size_t(g) * p.sigma * K) * L + j;   // + (code*K + band)*L
     const uint32_t* yw = reinterpret_cast<const uint32_t*>(p.ycode + c0r);
 
     uint32_t V[R];
@@ -624,7 +637,7 @@ comb2_kernel(const CombParams p) {
         for (int u = 0; u < 8; ++u) {
           uint32_t m[K][RRB];
 #pragma unroll
-          for (int b = 0; b < K; ++b) load_band_words<RRB>(tl + cd[b] * code_stride + size_t(b) * L * BW, m[b]);
+          for (int b = 0; b < K; ++b) load_band_words<RRB>(tblq, tblr, idx0 + (size_t(cd[b]) * K + b) * L, m[b]);
           uint32_t tinD[K], tinR[K];
           {
             const uint32_t shD = __shfl_up_sync(0xFFFFFFFFu, tbD[K - 1], 1, L);
