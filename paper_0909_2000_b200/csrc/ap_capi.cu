@@ -180,8 +180,12 @@ bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
     const int ctas = std::min({by_regs, by_smem, 16});
     if (ctas < 1) continue;
     const int warps = ctas * apk::kWarpsPerCta;
-    double cost = double(d.L) * (6.0 * d.RR + 16.0) + 50.0;
-    if (warps < 16) cost *= 16.0 / warps;
+    // per lane and raw column: 6 ALU ops per real row + ~30 fixed (shuffles,
+    // codes, extraction); the long-chain shapes hide latency with ILP, so only
+    // penalise occupancy below 8 warps per SM (fit to B200 sweeps, tools/shape_sweep2.sh)
+    double cost = double(d.L) * (6.0 * d.RR + 30.0) + 50.0;
+    if (warps < 8) cost *= 8.0 / warps;
+    cost *= d.K == 1 ? 1.0 : 1.02;
     if (cost < best) {
       best = cost;
       out->L = d.L;

@@ -500,26 +500,27 @@ comb_kernel(const CombParams p) {
 // table holds only real rows and real codes.  R = 2*RR blown rows per lane,
 // K bands of RRB = RR/K real rows; lanes j >= W/R (if any) are idle padding
 // whose output is never read (the bottom is lane W/R - 1's last band).
-// r = 2 table layout: per (group, code, band, lane) index idx the band's RRB
-// real-row words are split into Q4 = RRB/4 quads in tblq[idx*Q4 + q] (LDS.128)
-// and REM = RRB%4 (0..2) words in tblr[idx*REM + k] (LDS.64 / LDS.32): no
-// padding, every load naturally aligned.
+// r = 2 table layout: quads [code][band][quad][lane] (uint4) and the REM =
+// RRB % 4 (0..2) leftover words [code][band][lane] (uint32 / uint2), lane =
+// g*L + j.  For a fixed (band, quad) the 32 lanes read 32 consecutive 16-B
+// slots whatever code each lane holds: conflict-free LDS.128 for every L.
 __host__ __device__ constexpr int r2_band_words(int rrb) { return rrb; }
 
+// tq/tr point at this (code, band) block, already offset by the lane.
 template <int RRB>
-__device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t* tr, size_t idx, uint32_t* m) {
+__device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t* tr, uint32_t* m) {
   constexpr int Q4 = RRB / 4, REM = RRB % 4;
   static_assert(REM <= 2, "band real-row count must be 4q, 4q+1 or 4q+2");
 #pragma unroll
   for (int q = 0; q < Q4; ++q) {
-    const uint4 v = tq[idx * Q4 + q];
+    const uint4 v = tq[q * 32];
     m[4 * q] = v.x; m[4 * q + 1] = v.y; m[4 * q + 2] = v.z; m[4 * q + 3] = v.w;
   }
   if constexpr (REM == 2) {
-    const uint2 v = reinterpret_cast<const uint2*>(tr)[idx];
+    const uint2 v = *reinterpret_cast<const uint2*>(tr);
     m[4 * Q4] = v.x; m[4 * Q4 + 1] = v.y;
   } else if constexpr (REM == 1) {
-    m[4 * Q4] = tr[idx];
+    m[4 * Q4] = *tr;
   }
 }
 
@@ -541,9 +542,8 @@ comb2_kernel(const CombParams p) {
   const uint32_t j = lane % L;
   const size_t per_warp = comb_smem_per_warp(L, K * BW, p.sigma, p.ring, NB);
   unsigned char* wbase = smem + warp * per_warp;
-  const size_t nidx = size_t(G) * p.sigma * K * L;                     // (group, code, band, lane)
-  uint4* tblq = reinterpret_cast<uint4*>(wbase);                       // [nidx][Q4]
-  uint32_t* tblr = reinterpret_cast<uint32_t*>(tblq + nidx * Q4);      // [nidx][REM]
+  uint4* tblq = reinterpret_cast<uint4*>(wbase);                       // [sigma][K][Q4][32 lanes]
+  uint32_t* tblr = reinterpret_cast<uint32_t*>(tblq + size_t(p.sigma) * K * Q4 * 32);  // [sigma][K][32][REM]
   const size_t tbl_bytes = size_t(4) * 32 * p.sigma * K * BW;
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * (NB + 1);
   uint8_t* okA = wbase + tbl_bytes + G * (NB + 1) * 4 + size_t(g) * 2 * p.ring;
@@ -589,7 +589,7 @@ comb2_kernel(const CombParams p) {
       for (uint32_t a = 0; a < p.sigma; ++a) {
 #pragma unroll
         for (int b = 0; b < K; ++b) {
-          const size_t idx = ((size_t(g) * p.sigma + a) * K + b) * L + j;
+          const size_t ab = size_t(a) * K + b;
           uint32_t wv[RRB];
 #pragma unroll
           for (int i = 0; i < RRB; ++i) {
@@ -598,16 +598,17 @@ comb2_kernel(const CombParams p) {
           }
 #pragma unroll
           for (int q = 0; q < Q4; ++q)
-            tblq[idx * Q4 + q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+            tblq[(ab * Q4 + q) * 32 + lane] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
 #pragma unroll
-          for (int k = 0; k < REM; ++k) tblr[idx * REM + k] = wv[4 * Q4 + k];
+          for (int k = 0; k < REM; ++k) tblr[(ab * 32 + lane) * REM + k] = wv[4 * Q4 + k];
         }
       }
       for (uint32_t k = j; k < 2 * p.ring; k += L) okA[k] = 0;
     }
     __syncwarp();
 
-    const size_t idx0 = (size_t(g) * p.sigma * K) * L + j;   // + (code*K + band)*L
+    const uint4* tq0 = tblq + lane;
+    const uint32_t* tr0 = tblr + size_t(lane) * REM;
     const uint32_t* yw = reinterpret_cast<const uint32_t*>(p.ycode + c0r);
 
     uint32_t V[R];
@@ -637,7 +638,10 @@ comb2_kernel(const CombParams p) {
         for (int u = 0; u < 8; ++u) {
           uint32_t m[K][RRB];
 #pragma unroll
-          for (int b = 0; b < K; ++b) load_band_words<RRB>(tblq, tblr, idx0 + (size_t(cd[b]) * K + b) * L, m[b]);
+          for (int b = 0; b < K; ++b) {
+            const uint32_t ab = cd[b] * K + b;
+            load_band_words<RRB>(tq0 + ab * (Q4 * 32), tr0 + ab * (32 * REM), m[b]);
+          }
           uint32_t tinD[K], tinR[K];
           {
             const uint32_t shD = __shfl_up_sync(0xFFFFFFFFu, tbD[K - 1], 1, L);
