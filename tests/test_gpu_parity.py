@@ -156,3 +156,29 @@ def test_pgm_fused_matches_host_quantisation():
         rc, want = ol.plot_rows(x, y, w, h, r)
         g = ap.PlotGrid(want.shape[0], want.shape[1], w, h, values=want.reshape(-1))
         assert wr.plot_pgm(x, y, c) == wr.pgm_header(*want.shape) + wr.pgm_pixels(g, t).tobytes()
+
+
+def test_cli_matches_reference_cli_bytes():
+    """The CLI (python -m paper_0909_2000_b200) reproduces the reference CLI's output bytes
+    (tests/golden/cli, made by the reference library through oracle/ref_cli.cpp)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gdir = os.path.join(root, "tests", "golden", "cli")
+    index = json.load(open(os.path.join(gdir, "index.json")))
+    for case in index["cases"]:
+        args = [sys.executable, "-m", "paper_0909_2000_b200", "--x", os.path.join(gdir, "x.fa"), "--y",
+                os.path.join(gdir, "y.fa"), "--window", str(case["window"]), "--step", str(case["step"]),
+                "--format", case["format"]]
+        if case["lcs_only"]:
+            args.append("--lcs-only")
+        if case["dense"]:
+            args.append("--dense")
+        if case["threshold"] is not None:
+            args += ["--threshold", str(case["threshold"])]
+        out = subprocess.run(args, capture_output=True, cwd=root, timeout=300)
+        assert out.returncode == 0, out.stderr.decode()
+        want = open(os.path.join(gdir, case["file"]), "rb").read()
+        assert out.stdout == want, case["name"]

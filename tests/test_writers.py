@@ -47,3 +47,26 @@ def test_pgm():
     vals = rng.integers(0, 15, 28)
     g = grid(4, 7, 7, 3, vals)
     assert np.array_equal(wr.pgm_pixels(g).reshape(-1), (255 * vals + 7) // 14)
+
+
+def test_fasta_reader_matches_reference_cases():
+    # test_io.cpp:107-150
+    import pytest
+    from paper_0909_2000_b200.fasta import ParseError, read_fasta_bytes, select_record
+    one = read_fasta_bytes(b">s\nACGT\n")
+    assert [(r.header, bytes(r.sequence)) for r in one] == [("s", b"ACGT")]
+    two = read_fasta_bytes(b">a\nAC\nGT\n>b\nTT\n")
+    assert [(r.header, bytes(r.sequence)) for r in two] == [("a", b"ACGT"), ("b", b"TT")]
+    recs = read_fasta_bytes(b">s desc here\nacgt acgt\r\n  ttaa\n")
+    assert recs[0].header == "s desc here" and bytes(recs[0].sequence) == b"ACGTACGTTTAA"
+    for bad in (b"ACGT\n", b"", b"\n\n", b">a\n>b\nAC\n", b">a\nAC\n>b\n", b">a\nAC>GT\n", b">a\nAC\x01GT\n"):
+        with pytest.raises(ParseError):
+            read_fasta_bytes(bad, "test")
+    with pytest.raises(ParseError, match="test:2"):
+        read_fasta_bytes(b"\nACGT\n", "test")
+    recs = read_fasta_bytes(b">alpha one\nAA\n>beta two\nCC\n")
+    assert select_record(recs, "", "f").header == "alpha one"
+    assert select_record(recs, "beta", "f").header == "beta two"
+    assert select_record(recs, "beta two", "f").header == "beta two"
+    with pytest.raises(ParseError):
+        select_record(recs, "gamma", "f")
