@@ -49,6 +49,7 @@ from paper_0909_2000_b200.sharding import plan_row_shards, shard_x  # noqa: E402
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 INT_PEAK = os.path.join(ROOT, "profiles", "int_peak_r01.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
 
 
 def log(*a):
@@ -344,8 +345,17 @@ def run_engine(args, rank, world, local_rank):
     if peak_ops_clk:
         peak = props.multi_processor_count * peak_ops_clk * sm_mhz * 1e6 / 1e12
         achieved = cells_local * 3 / kern_max / 1e12
+        traffic = None
+        if os.path.exists(NCU_TRAFFIC):
+            with open(NCU_TRAFFIC) as f:
+                traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
+        cpc = cells_local / kern_max / (props.multi_processor_count * sm_mhz * 1e6)
+        ceiling = 64.0 / (0.75 if c.r == 2 else 1.0)
         roof = {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel_alu_bound": {"cells_per_clk_per_sm": cpc, "ceiling": ceiling, "frac": cpc / ceiling,
+                                     "what": "comb cells per SM clock vs this kernel's own ALU-pipe ceiling "
+                                             "(64 lane-ops/clk/SM at 2 ALU ops per cell pair; 0.75 per cell for r=2)"},
                 "basis": "3 int32 lane-ops per comb cell (SURVEY §8d), cells = rows*(w*r)*(n*r); peak = "
                          f"{props.multi_processor_count} SMs x {peak_ops_clk:.1f} measured lane-ops/clk/SM x "
                          f"{sm_mhz:.0f} MHz (median SM clock during the run)",
