@@ -356,7 +356,7 @@ comb_kernel(const CombParams p) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int rho = 4 * q + k;
-              wv[k] = (xa[rho] == a ? 0u : 0x00003C00u) | (xb[rho] == a ? 0u : 0x3C000000u);
+              wv[k] = (xa[rho] == a ? 0x00008000u : 0u) | (xb[rho] == a ? 0x80000000u : 0u);
             }
             tg[(a * Q + q) * L + j] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
           }
@@ -425,7 +425,7 @@ comb_kernel(const CombParams p) {
               if constexpr (XM) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                  m[k] = prmt_sign((xpair[b * RB + 4 * qq + k] ^ yrep) + 0x7FFF7FFFu, 0xBB99u);
+                  m[k] = ~((xpair[b * RB + 4 * qq + k] ^ yrep) + 0x7FFF7FFFu) & 0x80008000u;
               } else {
                 const uint4 w4 = nfq[b * QB + qq];
                 m[0] = w4.x; m[1] = w4.y; m[2] = w4.z; m[3] = w4.w;
@@ -433,13 +433,7 @@ comb_kernel(const CombParams p) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 uint32_t& v = V[b * RB + 4 * qq + k];
-                uint32_t tt;
-                if constexpr (XM) {
-                  tt = t & m[k];
-                } else {
-                  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(tt) : "r"(t), "r"(m[k]));
-                }
-                const uint32_t d = __vmaxu2(v, tt);
+                const uint32_t d = __viaddmax_s16x2(t, m[k], v);   // max(T + A, V): A = -32768 on a match
                 v = lop3_xor(v, t, d);
                 t = d;
               }
@@ -594,7 +588,7 @@ comb2_kernel(const CombParams p) {
 #pragma unroll
           for (int i = 0; i < RRB; ++i) {
             const int rr = b * RRB + i;
-            wv[i] = (xa[rr] == a ? 0u : 0x00003C00u) | (xb[rr] == a ? 0u : 0x3C000000u);
+            wv[i] = (xa[rr] == a ? 0x00008000u : 0u) | (xb[rr] == a ? 0x80000000u : 0u);
           }
 #pragma unroll
           for (int q = 0; q < Q4; ++q)
@@ -675,9 +669,7 @@ comb2_kernel(const CombParams p) {
               vs = __vminu2(vs, t);
               t = d0;
               uint32_t& vr = V[b * 2 * RRB + 2 * i + 1]; // real x real: table
-              uint32_t tt;
-              asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(tt) : "r"(t), "r"(m[b][i]));
-              const uint32_t d1 = __vmaxu2(vr, tt);
+              const uint32_t d1 = __viaddmax_s16x2(t, m[b][i], vr);
               vr = lop3_xor(vr, t, d1);
               t = d1;
             }
