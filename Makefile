@@ -2,7 +2,7 @@
 #   make -j4        -> paper_0909_2000_b200/libalignplot_b200.so + oracle/
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $(EXTRA_NVFLAGS)
 PKG := paper_0909_2000_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/libalignplot_b200.so

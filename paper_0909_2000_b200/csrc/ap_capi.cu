@@ -399,6 +399,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.W = W;
   p.N = uint32_t(N);
   p.sigma = spec ? sigma_y : (sh.xm ? 0 : sigma);
+  p.one = 1u;
+  p.minus_one = 0xFFFFFFFFu;
   p.sent_code = sent;
   p.S = uint32_t(S);
   p.nseg = uint32_t(nseg);

@@ -75,6 +75,8 @@ struct CombParams {
   unsigned long long stage_cap;
   uint32_t* seg_counts;           // [rows][nseg] hits per (row, segment)
   uint32_t zero;                  // always 0 (HFMA2 addend)
+  uint32_t one;                   // always 1 (IMAD forms the compiler must not fold)
+  uint32_t minus_one;             // always 0xFFFFFFFF
 };
 
 using KernelFn = void (*)(CombParams);
