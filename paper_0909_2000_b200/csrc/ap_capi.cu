@@ -144,6 +144,7 @@ constexpr Shape2Def kShapes2[] = {
     {4, 25, 5}, {8, 8, 2}, {8, 8, 4}, {16, 4, 2}, {16, 8, 4}, {32, 8, 4},
     {8, 16, 4}, {16, 16, 4}, {32, 16, 4}, {32, 4, 2},
     {8, 20, 4}, {16, 10, 2}, {32, 5, 1}, {4, 25, 1}, {32, 4, 1}, {16, 4, 1},
+    {10, 10, 2}, {5, 20, 4}, {10, 10, 1}, {5, 20, 1},
 };
 
 bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
@@ -183,9 +184,9 @@ bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
     // per lane and raw column: 6 ALU ops per real row + ~30 fixed (shuffles,
     // codes, extraction); the long-chain shapes hide latency with ILP, so only
     // penalise occupancy below 8 warps per SM (fit to B200 sweeps, tools/shape_sweep2.sh)
-    double cost = double(d.L) * (6.0 * d.RR + 30.0) + 50.0;
-    if (warps < 8) cost *= 8.0 / warps;
-    cost *= d.K == 1 ? 1.0 : 1.02;
+    const double lanes_per_group = 32.0 / (32 / d.L);   // idle lanes of a non-dividing L count too
+    double cost = lanes_per_group * (6.0 * d.RR + 30.0) + 50.0;
+    if (warps < 16) cost *= 16.0 / warps;
     if (cost < best) {
       best = cost;
       out->L = d.L;

@@ -16,6 +16,7 @@ KernelFn pick_r2(int l, int rr, int k, bool dense) {
   AP_R2(4, 25, 5) AP_R2(8, 8, 2) AP_R2(8, 8, 4) AP_R2(16, 4, 2) AP_R2(16, 8, 4) AP_R2(32, 8, 4)
   AP_R2(8, 16, 4) AP_R2(16, 16, 4) AP_R2(32, 16, 4) AP_R2(32, 4, 2)
   AP_R2(8, 20, 4) AP_R2(16, 10, 2) AP_R2(32, 5, 1) AP_R2(4, 25, 1) AP_R2(32, 4, 1) AP_R2(16, 4, 1)
+  AP_R2(10, 10, 2) AP_R2(5, 20, 4) AP_R2(10, 10, 1) AP_R2(5, 20, 1)
 #undef AP_R2
   return nullptr;
 }

@@ -89,6 +89,32 @@ KernelFn pick_r2(int l, int rr, int k, bool dense);
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Lane groups.  L lanes comb one strip pair; G = 32 / L groups per warp.  When
+// L does not divide 32 the trailing 32 - G*L lanes form an idle "phantom"
+// group (no strips, own scratch) so every lane runs the same code.  Shuffles
+// are full-width: a group's lane 0 always overrides what it receives, and scans
+// only accumulate from lanes of the same group (j >= off).
+__host__ __device__ constexpr int groups_per_warp(int L) { return 32 / L; }
+__host__ __device__ constexpr int groups_alloc(int L) { return 32 / L + (32 % L ? 1 : 0); }
+__host__ __device__ constexpr int ring_stride(int L, int nb) { return L * ((nb + L - 1) / L) + 1; }
+
+template <int L>
+__device__ __forceinline__ uint32_t shfl_up1(uint32_t v) {
+  if constexpr ((L & (L - 1)) == 0) return __shfl_up_sync(0xFFFFFFFFu, v, 1, L);
+  else return __shfl_up_sync(0xFFFFFFFFu, v, 1);
+}
+template <int L>
+__device__ __forceinline__ uint32_t shfl_up_n(uint32_t v, int off) {
+  if constexpr ((L & (L - 1)) == 0) return __shfl_up_sync(0xFFFFFFFFu, v, off, L);
+  else return __shfl_up_sync(0xFFFFFFFFu, v, off);
+}
+// value of the group's last lane
+template <int L>
+__device__ __forceinline__ uint32_t shfl_group_last(uint32_t v, uint32_t g) {
+  if constexpr ((L & (L - 1)) == 0) return __shfl_sync(0xFFFFFFFFu, v, L - 1, L);
+  else return __shfl_sync(0xFFFFFFFFu, v, (g * L + L - 1) & 31u);
+}
+
 __device__ __forceinline__ uint32_t lop3_xor(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -108,10 +134,10 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t sel) {
 // the ok-flag rings.
 __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uint32_t sigma, uint32_t ring,
                                                      int nb = kChunk) {
-  const int G = 32 / L;
+  const int Ga = groups_alloc(L);
   const size_t bytes = size_t(4) * 32 * sigma * table_words   // mismatch table (sigma = 0: computed masks)
-       + size_t(G) * (nb + 1) * 4                              // bottom-key ring per group
-       + size_t(G) * 2 * ring;                                 // ok flags per group (strip A, strip B)
+       + size_t(Ga) * ring_stride(L, nb) * 4                   // bottom-key ring per group (padded)
+       + size_t(Ga) * 2 * ring;                                // ok flags per group (strip A, strip B)
   return (bytes + 15) & ~size_t(15);                           // keep every warp's table 16-B aligned
 }
 
@@ -134,13 +160,13 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
                                               uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
   const uint32_t rmask = p.ring - 1;
   const uint32_t rshift = p.r - 1;
-  constexpr int CPL = NB / L;
+  constexpr int CPL = (NB + L - 1) / L;   // columns per lane (the last lane may get fewer real ones)
   const int32_t eb = E0 + int32_t(j) * CPL;
   uint32_t cmask = 0;   // bit 2c: strip A countable, bit 2c+1: strip B
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = e >= 0 && e < int32_t(nseg_cols);
+    const bool valid = e >= 0 && e < int32_t(nseg_cols) && (NB % L == 0 || j * CPL + c < NB);
     const uint32_t k = ringB[j * CPL + c];
     const int32_t thr = e - kbase - int32_t(p.W);
     const int32_t kA = int32_t(k & 0xFFFFu), kB = int32_t(k >> 16);
@@ -156,7 +182,7 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = e >= 0 && e < int32_t(nseg_cols);
+    const bool valid = e >= 0 && e < int32_t(nseg_cols) && (NB % L == 0 || j * CPL + c < NB);
     uint32_t oA = 0, oB = 0;
     if (valid) {
       const uint32_t slot = uint32_t(e - int32_t(p.W)) & rmask;
@@ -173,7 +199,7 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
   uint32_t incl = acc;
 #pragma unroll
   for (int off = 1; off < L; off <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off, L);
+    const uint32_t v = shfl_up_n<L>(incl, off);
     if (j >= uint32_t(off)) incl += v;
   }
   const uint32_t excl = incl - acc;
@@ -183,7 +209,7 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = e >= 0 && e < int32_t(nseg_cols);
+    const bool valid = e >= 0 && e < int32_t(nseg_cols) && (NB % L == 0 || j * CPL + c < NB);
     const uint32_t cnt = run + excl + dl[c] - bias0 - uint32_t(c + 1) * 0x00010001u;
     const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
     const bool out_ok = valid && kp >= 0 && kp < int32_t(p.S) && !(uint32_t(kp) & rshift);
@@ -221,11 +247,11 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
       uint32_t gi = pk;
 #pragma unroll
       for (int off = 1; off < L; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, gi, off, L);
+        const uint32_t v = shfl_up_n<L>(gi, off);
         if (j >= uint32_t(off)) gi += v;
       }
       const uint32_t gex = gi - pk;
-      const uint32_t gtot = __shfl_sync(0xFFFFFFFFu, gi, L - 1, L);
+      const uint32_t gtot = shfl_group_last<L>(gi, g);
       uint32_t wi = nA + nB;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -255,7 +281,7 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
       hitsB += gtot >> 16;
     }
   }
-  run = __shfl_sync(0xFFFFFFFFu, run + incl - (j + 1) * CPL * 0x00010001u, L - 1, L);
+  run = shfl_group_last<L>(run + incl - (j + 1) * CPL * 0x00010001u, g);
   __syncwarp();
 }
 
@@ -411,7 +437,7 @@ comb_kernel(const CombParams p) {
           // seaweeds entering each band
           uint32_t tin[K];
           {
-            const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, tb[K - 1], 1, L);
+            const uint32_t sh = shfl_up1<L>(tb[K - 1]);
             tin[0] = j == 0 ? fresh : sh;
 #pragma unroll
             for (int b = 1; b < K; ++b) tin[b] = tb[b - 1];
@@ -447,7 +473,7 @@ comb_kernel(const CombParams p) {
           {
             const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
             const uint32_t ynew = (ww >> (8 * ((u + 1) & 3))) & 0xFFu;
-            const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, cd[K - 1], 1, L);
+            const uint32_t sh = shfl_up1<L>(cd[K - 1]);
 #pragma unroll
             for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
             cd[0] = j == 0 ? ynew : sh;
@@ -523,8 +549,8 @@ __device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t*
 template <int L, int RR, int K, bool DENSE>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= 8 ? 4 : (RR <= 16 ? 3 : 2))
 comb2_kernel(const CombParams p) {
-  static_assert(32 % L == 0 && RR % K == 0, "bad shape");
-  constexpr int G = 32 / L;
+  static_assert(L <= 32 && RR % K == 0, "bad shape");
+  constexpr int G = groups_per_warp(L);     // real groups; lanes >= G*L are idle
   constexpr int R = 2 * RR;
   constexpr int RRB = RR / K;
   constexpr int BW = r2_band_words(RRB);
@@ -541,8 +567,9 @@ comb2_kernel(const CombParams p) {
   uint4* tblq = reinterpret_cast<uint4*>(wbase);                       // [sigma][K][Q4][32 lanes]
   uint32_t* tblr = reinterpret_cast<uint32_t*>(tblq + size_t(p.sigma) * K * Q4 * 32);  // [sigma][K][32][REM]
   const size_t tbl_bytes = size_t(4) * 32 * p.sigma * K * BW;
-  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * (NB + 1);
-  uint8_t* okA = wbase + tbl_bytes + G * (NB + 1) * 4 + size_t(g) * 2 * p.ring;
+  constexpr int RS = ring_stride(L, NB);
+  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * RS;
+  uint8_t* okA = wbase + tbl_bytes + groups_alloc(L) * RS * 4 + size_t(g) * 2 * p.ring;
   uint8_t* okB = okA + p.ring;
 
   const uint32_t lanes_real = p.W / R;          // host guarantees W % R == 0, lanes_real <= L
@@ -557,7 +584,7 @@ comb2_kernel(const CombParams p) {
     const uint32_t seg = uint32_t(task % p.nseg);
     const uint32_t pair = pg * G + g;
     const uint32_t rA = 2 * pair, rB = 2 * pair + 1;
-    const bool hasA = rA < p.rows, hasB = rB < p.rows;
+    const bool hasA = g < uint32_t(G) && rA < p.rows, hasB = g < uint32_t(G) && rB < p.rows;
     const uint32_t c0 = seg * p.S;                         // blown, multiple of 64
     const uint32_t c0r = c0 >> 1;                          // raw, multiple of 32
     const uint32_t nseg_cols = min(p.S + p.W - 1, p.N - c0);
@@ -640,8 +667,8 @@ comb2_kernel(const CombParams p) {
           }
           uint32_t tinD[K], tinR[K];
           {
-            const uint32_t shD = __shfl_up_sync(0xFFFFFFFFu, tbD[K - 1], 1, L);
-            const uint32_t shR = __shfl_up_sync(0xFFFFFFFFu, tbR[K - 1], 1, L);
+            const uint32_t shD = shfl_up1<L>(tbD[K - 1]);
+            const uint32_t shR = shfl_up1<L>(tbR[K - 1]);
             tinD[0] = j == 0 ? fresh : shD;
             tinR[0] = j == 0 ? fresh + 0x00010001u : shR;
 #pragma unroll
@@ -684,7 +711,7 @@ comb2_kernel(const CombParams p) {
           {
             const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
             const uint32_t ynew = (ww >> (8 * ((u + 1) & 3))) & 0xFFu;
-            const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, cd[K - 1], 1, L);
+            const uint32_t sh = shfl_up1<L>(cd[K - 1]);
 #pragma unroll
             for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
             cd[0] = j == 0 ? ynew : sh;

@@ -182,3 +182,36 @@ def test_cli_matches_reference_cli_bytes():
         assert out.returncode == 0, out.stderr.decode()
         want = open(os.path.join(gdir, case["file"]), "rb").read()
         assert out.stdout == want, case["name"]
+
+
+@pytest.mark.parametrize("shape", ["8,8,2", "8,16,2", "8,16,4", "16,16,4", "32,8,2", "32,32,4", "16,24,2"])
+def test_forced_generic_shapes(shape, monkeypatch):
+    """Every instantiated generic (L, R, K) shape, forced with AP_SHAPE, is bit-exact."""
+    monkeypatch.setenv("AP_SHAPE", shape)
+    monkeypatch.setenv("AP_NO_R2", "1")
+    rng = np.random.default_rng(hash(shape) & 0xFFFF)
+    L, R, K = map(int, shape.split(","))
+    for r in (1, 2):
+        w = max(2, min((L * R) // r - 3, 200))
+        x = rng.integers(1, 5, w + 150).astype(np.uint8)
+        y = rng.integers(1, 5, w + 700).astype(np.uint8)
+        rc, want = ol.plot_rows(x, y, w, 2, r)
+        assert np.array_equal(gpu_grid(x, y, w, 2, r), want), (shape, r)
+
+
+@pytest.mark.parametrize("shape", ["4,25,5", "4,25,1", "10,10,2", "10,10,1", "5,20,4", "5,20,1", "8,8,2",
+                                   "16,4,2", "32,4,2", "16,10,2", "8,20,4", "32,5,1"])
+def test_forced_r2_shapes(shape, monkeypatch):
+    """Every instantiated r = 2 (L, RR, K) shape, forced with AP_SHAPE2, is bit-exact (dense and threshold)."""
+    monkeypatch.setenv("AP_SHAPE2", shape)
+    L, RR, K = map(int, shape.split(","))
+    w = RR * min(L, max(1, 100 // RR))
+    rng = np.random.default_rng(RR * 131 + L)
+    x = rng.integers(1, 5, w + 120).astype(np.uint8)
+    y = np.concatenate([x[10:w + 60], rng.integers(1, 5, 600)]).astype(np.uint8)
+    rc, want = ol.plot_rows(x, y, w, 1, 2)
+    assert np.array_equal(gpu_grid(x, y, w, 1, 2), want), shape
+    t = int(np.quantile(want, 0.95))
+    rr, cc = np.nonzero(want >= t)
+    gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
+    assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape
