@@ -327,6 +327,28 @@ def run_engine(args, rank, world, local_rank):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te[0])
     d2h = rows_local * cols * 2 if dense else hits_local * 10 + 8
+    # the same through ap_plot_dense_u8 (lossless bytes for w <= 127): half the D2H
+    e2e_u8 = None
+    if dense and c.w <= 127:
+        hout8 = torch.empty(rows_local * cols, dtype=torch.uint8).pin_memory()
+
+        def e2e_u8_step():
+            rc = L.ap_plot_dense_u8(hx.data_ptr(), xs.size, hy.data_ptr(), n, ctypes.byref(apc), hout8.data_ptr())
+            if rc:
+                raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
+
+        e2e_u8_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_u8_step()
+        te8 = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te8, op=dist.ReduceOp.MAX)
+        e2e_u8 = {"value": rows_global * cols * c.w * args.steps / float(te8[0]), "unit": "window-pair cell updates/s",
+                  "h2d_bytes_per_step": int(xs.size + n), "d2h_bytes_per_step": int(rows_local * cols),
+                  "api": "ap_plot_dense_u8 (half-unit scores as bytes, lossless for w <= 127)"}
 
     if rank != 0:
         L.ap_ctx_destroy(ctx)
@@ -387,6 +409,7 @@ def run_engine(args, rank, world, local_rank):
         "roofline": roof, "roofline_hbm_output": hbm, "clocks": clocks,
         "e2e": {"value": wpcu * args.steps / t_e2e, "unit": "window-pair cell updates/s",
                 "h2d_bytes_per_step": int(xs.size + n), "d2h_bytes_per_step": int(d2h)},
+        "e2e_compact": e2e_u8,
         "gpu_launches": launches, "cpu_baseline": cpu,
     }
     if not dense:

@@ -82,6 +82,12 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
                       uint64_t* count, uint32_t* rows, uint32_t* cols, uint16_t* halves,
                       size_t cap);
 
+/* As ap_plot_dense with the half-unit scores stored as bytes (lossless for
+ * w <= 127, where scores lie in [0, 2w]; AP_CONFIG otherwise): half the
+ * device-to-host bytes of the uint16 layout. */
+int ap_plot_dense_u8(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                     uint8_t* out_half);
+
 /* Dense 8-bit PGM raster of rows [row_begin, row_end), the pixels of
  * write_pgm (io.cpp:136-153) quantised inside the comb kernel:
  * pixel = (255 * clamp(half, 0, 2w) + w) / (2w), and, when has_threshold,
@@ -107,6 +113,10 @@ int ap_ctx_destroy(ap_ctx* ctx);
  * Sentinel bytes are not checked (the host API checks them). */
 int ap_ctx_plot_dense_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y,
                              size_t n, const ap_config* cfg, uint16_t* d_out, void* stream);
+
+/* As ap_plot_dense_u8 on device pointers (enqueue only). */
+int ap_ctx_plot_dense_u8_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                                const ap_config* cfg, uint8_t* d_out, void* stream);
 
 /* As ap_plot_pgm on device pointers (enqueue only). */
 int ap_ctx_plot_pgm_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,

@@ -20,9 +20,11 @@ AP_MAX_BLOWN_WINDOW = 1024
 
 # Every symbol declared in include/alignplot_b200.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "ap_grid_dims", "ap_validate", "ap_plot_dense", "ap_plot_threshold", "ap_plot_pgm", "ap_last_error",
+    "ap_grid_dims", "ap_validate", "ap_plot_dense", "ap_plot_dense_u8", "ap_plot_threshold", "ap_plot_pgm",
+    "ap_last_error",
     "ap_device_count", "ap_ctx_create", "ap_ctx_destroy", "ap_ctx_plot_dense_device",
-    "ap_ctx_plot_threshold_device", "ap_ctx_plot_pgm_device", "ap_ctx_last_kernel_ms", "ap_ctx_last_launches",
+    "ap_ctx_plot_threshold_device", "ap_ctx_plot_pgm_device", "ap_ctx_plot_dense_u8_device",
+    "ap_ctx_last_kernel_ms", "ap_ctx_last_launches",
 )
 
 
@@ -62,6 +64,11 @@ def lib() -> ctypes.CDLL:
     L.ap_plot_threshold.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig),
                                     POINTER(c_uint64), c_void_p, c_void_p, c_void_p, c_size_t]
     L.ap_plot_threshold.restype = c_int
+    L.ap_plot_dense_u8.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig), c_void_p]
+    L.ap_plot_dense_u8.restype = c_int
+    L.ap_ctx_plot_dense_u8_device.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t,
+                                              POINTER(ApConfig), c_void_p, c_void_p]
+    L.ap_ctx_plot_dense_u8_device.restype = c_int
     L.ap_plot_pgm.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig), c_void_p]
     L.ap_plot_pgm.restype = c_int
     L.ap_ctx_plot_pgm_device.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig),

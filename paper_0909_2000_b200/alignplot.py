@@ -290,6 +290,17 @@ def plot_dense_u16(x, y, cfg: PlotConfig, row_begin: int = 0, row_end: int = 0) 
     return out
 
 
+def plot_dense_u8(x, y, cfg: PlotConfig, row_begin: int = 0, row_end: int = 0) -> np.ndarray:
+    """Dense half-unit grid as bytes (w <= 127) via ap_plot_dense_u8: half the D2H of uint16."""
+    xa, ya = _codes(x), _codes(y)
+    rows, cols = window_grid_dims(xa.size, ya.size, cfg.window_w, cfg.step_h)
+    re = rows if row_end == 0 else min(row_end, rows)
+    out = np.empty((max(re - row_begin, 0), cols), dtype=np.uint8)
+    _raise(_native.lib().ap_plot_dense_u8(_ptr(xa), xa.size, _ptr(ya), ya.size,
+                                          ctypes.byref(_cfg(cfg, row_begin, row_end)), _ptr(out)))
+    return out
+
+
 def compute_plot(x: Sequence, y: Sequence, cfg: PlotConfig) -> PlotGrid:
     """runner.cpp:78-131 on the CUDA engine: validate first, then the dense grid (int32 half-units)."""
     cfg.validate(x.size(), y.size())

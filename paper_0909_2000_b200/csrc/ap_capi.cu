@@ -210,8 +210,11 @@ struct ap_ctx {
   int sms = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream_copy = nullptr;   // D2H of finished row blocks (overlaps the comb kernel)
+  cudaStream_t stream_b = nullptr;      // second compute stream: consecutive row blocks overlap
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t ev_blk[8] = {};
+  static constexpr int kMaxBlocks = 32;
+  cudaEvent_t ev_blk[kMaxBlocks] = {};
+  cudaEvent_t ev_aux[2] = {};
   std::mutex mu;
   // scratch (grown on demand)
   uint8_t *d_x = nullptr, *d_y = nullptr, *d_xcode = nullptr, *d_ycode = nullptr, *d_map = nullptr;
@@ -438,33 +441,41 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   CK(cudaEventRecord(c->ev0, st));
   if (dense && host_out) {
-    // Dense output to the host: launch the plot as row blocks of about one
-    // wave each and stream every finished block's D2H on the copy stream, so
-    // the PCIe transfer overlaps the comb kernel of the next block.
-    const size_t waves = (ntasks + total_warps - 1) / total_warps;
-    const size_t nblk = std::min<size_t>(std::max<size_t>(waves, 1), 8);
+    // Dense output to the host: launch the plot as ~16 row blocks alternating
+    // over two compute streams (consecutive blocks overlap, so small blocks do
+    // not leave the GPU idle) and stream every finished block's D2H on the copy
+    // stream, so the PCIe transfer hides under the comb kernels of later blocks.
+    // blocks of at least half a wave each (two run concurrently), at most 16
+    const size_t nblk = std::min<size_t>({std::max<size_t>(ntasks / std::max<size_t>(total_warps / 2, 1), 1),
+                                          std::max<size_t>(ngroups, 1), 16});
     const size_t gpb = (ngroups + nblk - 1) / nblk;          // pair groups per block
-    const size_t elem = out_kind == 1 ? 1 : 2;
+    const size_t elem = out_kind == 0 ? 2 : 1;
+    CK(cudaEventRecord(c->ev_aux[0], st));                   // code streams ready
+    CK(cudaStreamWaitEvent(c->stream_b, c->ev_aux[0], 0));
+    size_t launched = 0;
     for (size_t k = 0; k < nblk; ++k) {
       const size_t r0 = std::min(nrows, k * gpb * 2 * G), r1 = std::min(nrows, (k + 1) * gpb * 2 * G);
       if (r0 >= r1) break;
+      cudaStream_t sk = (k & 1) ? c->stream_b : st;
       apk::CombParams pk = p;
       pk.xcode = c->d_xcode + r0 * h;
       pk.rows = uint32_t(r1 - r0);
       pk.row_global0 = uint32_t(row_global0 + r0);
-      pk.out = p.out + (out_kind == 1 ? 0 : r0 * cols);
-      pk.out8 = p.out8 + (out_kind == 1 ? r0 * cols : 0);
+      pk.out = p.out + (out_kind == 0 ? r0 * cols : 0);
+      pk.out8 = p.out8 + (out_kind == 0 ? 0 : r0 * cols);
       const size_t tk = ((r1 - r0 + 1) / 2 + G - 1) / G * nseg;
       const size_t gk = std::min<size_t>((tk + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta, size_t(c->sms) * per_sm);
-      fn<<<dim3(unsigned(gk)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(pk);
+      fn<<<dim3(unsigned(gk)), dim3(apk::kWarpsPerCta * 32), sh.smem, sk>>>(pk);
       CK(cudaGetLastError());
-      CK(cudaEventRecord(c->ev_blk[k], st));
+      CK(cudaEventRecord(c->ev_blk[k], sk));
       c->last_launches += 1;
+      ++launched;
     }
+    CK(cudaEventRecord(c->ev_aux[1], c->stream_b));          // join the second stream
+    CK(cudaStreamWaitEvent(st, c->ev_aux[1], 0));
     CK(cudaEventRecord(c->ev1, st));
-    for (size_t k = 0; k < nblk; ++k) {
+    for (size_t k = 0; k < launched; ++k) {
       const size_t r0 = std::min(nrows, k * gpb * 2 * G), r1 = std::min(nrows, (k + 1) * gpb * 2 * G);
-      if (r0 >= r1) break;
       CK(cudaStreamWaitEvent(c->stream_copy, c->ev_blk[k], 0));
       CK(cudaMemcpyAsync(static_cast<char*>(host_out) + r0 * cols * elem,
                          static_cast<const char*>(d_out) + r0 * cols * elem, (r1 - r0) * cols * elem,
@@ -563,7 +574,9 @@ int ap_ctx_create(int device, ap_ctx** out) {
   c->sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->stream_b, cudaStreamNonBlocking));
   for (auto& e : c->ev_blk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : c->ev_aux) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
   CK(cudaMalloc(&c->d_small, 64));
@@ -595,8 +608,11 @@ int ap_ctx_destroy(ap_ctx* c) {
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
   for (auto& e : c->ev_blk) cudaEventDestroy(e);
+  for (auto& e : c->ev_aux) cudaEventDestroy(e);
+  cudaStreamSynchronize(c->stream_b);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->stream_copy);
+  cudaStreamDestroy(c->stream_b);
   delete c;
   return AP_OK;
 }
@@ -628,6 +644,24 @@ int ap_ctx_plot_dense_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint
   const size_t off = rb * cfg->step_h;
   return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr,
                     nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+int ap_ctx_plot_dense_u8_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                                const ap_config* cfg, uint8_t* d_out, void* stream) {
+  if (!c || !d_x || !d_y || !d_out) return fail(AP_INVALID, "null argument");
+  int rc = check_cfg(m, n, cfg);
+  if (rc) return rc;
+  if (cfg->window_w > 127)
+    return fail(AP_CONFIG, "uint8 half-units need w <= 127 (scores up to 2w), got w = %zu", size_t(cfg->window_w));
+  size_t rows, cols, rb, re;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
+  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DevGuard dg(c->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const size_t off = rb * cfg->step_h;
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr,
+                    nullptr, nullptr, nullptr, nullptr, 0, 2);
 }
 
 int ap_ctx_plot_pgm_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
@@ -687,7 +721,7 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
   if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
   if (dense && !out_dense && re > rb) return fail(AP_INVALID, "null output");
-  const size_t out_elem = out_kind == 1 ? 1 : 2;
+  const size_t out_elem = out_kind == 0 ? 2 : 1;
   const int ndev_avail = ap_device_count();
   if (ndev_avail <= 0) return fail(AP_NODEV, "no CUDA device available (the engine has no CPU fallback)");
   int ndev = cfg->n_devices <= 1 ? 1 : std::min(cfg->n_devices, ndev_avail);
@@ -803,6 +837,18 @@ int ap_plot_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const 
 int ap_plot_pgm(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                 uint8_t* pixels) {
   return host_plot(x, m, y, n, cfg, true, pixels, nullptr, nullptr, nullptr, nullptr, 0, 1);
+}
+
+int ap_plot_dense_u8(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                     uint8_t* out_half) {
+  if (cfg && cfg->window_w > 127)
+    return fail(AP_CONFIG, "uint8 half-units need w <= 127 (scores up to 2w), got w = %zu", size_t(cfg->window_w));
+  if (cfg && cfg->has_threshold) {
+    ap_config c = *cfg;
+    c.has_threshold = 0;
+    return host_plot(x, m, y, n, &c, true, out_half, nullptr, nullptr, nullptr, nullptr, 0, 2);
+  }
+  return host_plot(x, m, y, n, cfg, true, out_half, nullptr, nullptr, nullptr, nullptr, 0, 2);
 }
 
 int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,

@@ -65,7 +65,7 @@ struct CombParams {
   // dense output
   uint16_t* out;          // [rows][cols] half-units (out_kind 0)
   uint8_t* out8;          // [rows][cols] PGM pixels (out_kind 1, io.cpp:136-153 fused)
-  uint32_t out_kind;      // 0 = uint16 half-units, 1 = uint8 PGM pixels
+  uint32_t out_kind;      // 0 = uint16 half-units, 1 = uint8 PGM pixels, 2 = uint8 half-units
   int32_t pgm_threshold;  // cells below it render 0 (when has_pgm_threshold)
   uint32_t has_pgm_threshold;
   // thresholded output
@@ -222,6 +222,9 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
       if (p.out_kind == 0) {
         if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
         if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
+      } else if (p.out_kind == 2) {   // compact: half-units as bytes (w <= 127)
+        if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(hA);
+        if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(hB);
       } else {
         // write_pgm (io.cpp:136-153): pixel = (255*clamp(h,0,2w) + w) / 2w, cut -> 0
         const int32_t full = 2 * int32_t(p.w);

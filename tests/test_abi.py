@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "alignplot_b200.h")
 
 def declared_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(ap_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ap_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_and_binding_agree():
@@ -61,3 +61,16 @@ def test_validate_host_only():
     assert v(50, 200, 100, 5, 2) == _native.AP_EMPTY
     assert v(2000, 2000, 513, 1, 2) == _native.AP_CONFIG  # engine limit: w*r <= 1024
     assert v(2000, 2000, 512, 1, 2) == 0
+
+
+def test_cpp_shim_compiles():
+    """The C++ drop-in header compiles against the C ABI (linking happens in the GPU test)."""
+    import shutil
+    import subprocess
+    import tempfile
+    if not shutil.which("g++"):
+        pytest.skip("g++ unavailable")
+    with tempfile.TemporaryDirectory() as d:
+        res = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", os.path.join(ROOT, "tests", "cpp", "test_shim.cpp")],
+                             capture_output=True, text=True, cwd=d)
+        assert res.returncode == 0, res.stderr

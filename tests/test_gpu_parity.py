@@ -215,3 +215,14 @@ def test_forced_r2_shapes(shape, monkeypatch):
     rr, cc = np.nonzero(want >= t)
     gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape
+
+
+def test_dense_u8_matches_u16():
+    rng = np.random.default_rng(8)
+    x = rng.integers(1, 5, 600).astype(np.uint8)
+    y = np.concatenate([x[50:350], rng.integers(1, 5, 400)]).astype(np.uint8)
+    for w, h, r in ((100, 1, 2), (127, 2, 1), (30, 3, 2)):
+        c = cfg(w, h, r)
+        assert np.array_equal(ap.plot_dense_u8(x, y, c).astype(np.int32), gpu_grid(x, y, w, h, r))
+    with pytest.raises(ap.ConfigError):
+        ap.plot_dense_u8(x, y, cfg(128, 1, 1))
