@@ -722,7 +722,12 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
   if (dense && !out_dense && re > rb) return fail(AP_INVALID, "null output");
   const size_t out_elem = out_kind == 0 ? 2 : 1;
-  const int ndev_avail = ap_device_count();
+  const int ndev_real = ap_device_count();
+  // AP_SHARDS_PER_DEVICE=k (testing): let one physical GPU stand in for k shard
+  // devices, so the multi-device split/gather path runs on a single-GPU box.
+  int per_dev = 1;
+  if (const char* env = std::getenv("AP_SHARDS_PER_DEVICE")) per_dev = std::max(1, std::atoi(env));
+  const int ndev_avail = ndev_real * per_dev;
   if (ndev_avail <= 0) return fail(AP_NODEV, "no CUDA device available (the engine has no CPU fallback)");
   int ndev = cfg->n_devices <= 1 ? 1 : std::min(cfg->n_devices, ndev_avail);
   int cur = 0;
@@ -736,10 +741,14 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
     size_t total = 0;
     int rc = AP_OK;
     std::string err;
+    // multi-shard threshold lists are staged on the host inside the shard's
+    // context lock (shards may share a device context)
+    std::vector<uint32_t> hr, hc;
+    std::vector<uint16_t> hh;
   };
   std::vector<Shard> sh(ndev);
   for (int d = 0; d < ndev; ++d) {
-    sh[d].dev = ndev == 1 ? cur : d;
+    sh[d].dev = ndev == 1 ? cur : d % std::max(ndev_real, 1);
     sh[d].r0 = rb + nr * d / ndev;
     sh[d].r1 = rb + nr * (d + 1) / ndev;
   }
@@ -781,6 +790,15 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
           return q;
         CK(cudaStreamSynchronize(st));
         s.total = total;
+        if (ndev > 1 && total) {
+          const size_t k = std::min(total, need);
+          s.hr.resize(k);
+          s.hc.resize(k);
+          s.hh.resize(k);
+          CK(cudaMemcpy(s.hr.data(), c->d_orow, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+          CK(cudaMemcpy(s.hc.data(), c->d_ocol, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+          CK(cudaMemcpy(s.hh.data(), c->d_ohalf, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+        }
       }
       return AP_OK;
     };
@@ -808,11 +826,17 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   if (count) *count = total;
   for (int d = 0; d < ndev; ++d) {
     if (offs[d] >= cap || sh[d].total == 0) continue;
+    const size_t k = std::min<size_t>(sh[d].total, cap - offs[d]);
+    if (ndev > 1) {
+      std::memcpy(orow + offs[d], sh[d].hr.data(), k * sizeof(uint32_t));
+      std::memcpy(ocol + offs[d], sh[d].hc.data(), k * sizeof(uint32_t));
+      std::memcpy(ohalf + offs[d], sh[d].hh.data(), k * sizeof(uint16_t));
+      continue;
+    }
     ap_ctx* c = nullptr;
     get_ctx(sh[d].dev, &c);
     std::lock_guard<std::mutex> lk(c->mu);
     DevGuard dg(c->device);
-    const size_t k = std::min<size_t>(sh[d].total, cap - offs[d]);
     CK(cudaMemcpy(orow + offs[d], c->d_orow, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(ocol + offs[d], c->d_ocol, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(ohalf + offs[d], c->d_ohalf, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));

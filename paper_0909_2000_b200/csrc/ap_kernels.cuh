@@ -97,6 +97,9 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __host__ __device__ constexpr int groups_per_warp(int L) { return 32 / L; }
 __host__ __device__ constexpr int groups_alloc(int L) { return 32 / L + (32 % L ? 1 : 0); }
 __host__ __device__ constexpr int ring_stride(int L, int nb) { return L * ((nb + L - 1) / L) + 1; }
+// ok-flag bytes per group: two rings (strips A, B) plus 32 bytes of padding so
+// the same slot of different groups falls in different banks (8 banks apart).
+__host__ __device__ constexpr size_t ok_stride(uint32_t ring) { return size_t(2) * ring + 32; }
 
 template <int L>
 __device__ __forceinline__ uint32_t shfl_up1(uint32_t v) {
@@ -137,7 +140,7 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
   const int Ga = groups_alloc(L);
   const size_t bytes = size_t(4) * 32 * sigma * table_words   // mismatch table (sigma = 0: computed masks)
        + size_t(Ga) * ring_stride(L, nb) * 4                   // bottom-key ring per group (padded)
-       + size_t(Ga) * 2 * ring;                                // ok flags per group (strip A, strip B)
+       + size_t(Ga) * ok_stride(ring);                         // ok flags per group (strip A, strip B)
   return (bytes + 15) & ~size_t(15);                           // keep every warp's table 16-B aligned
 }
 
@@ -329,7 +332,7 @@ comb_kernel(const CombParams p) {
   unsigned char* wbase = smem + warp * per_warp;
   uint4* tbl = reinterpret_cast<uint4*>(wbase);                       // [G][sigma][Q][L]
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + size_t(128) * p.sigma * R) + g * (kChunk + 1);
-  uint8_t* okA = wbase + size_t(128) * p.sigma * R + G * (kChunk + 1) * 4 + size_t(g) * 2 * p.ring;
+  uint8_t* okA = wbase + size_t(128) * p.sigma * R + G * (kChunk + 1) * 4 + size_t(g) * ok_stride(p.ring);
   uint8_t* okB = okA + p.ring;
   const uint32_t rmask = p.ring - 1;
   const uint32_t rshift = p.r - 1;
@@ -572,7 +575,7 @@ comb2_kernel(const CombParams p) {
   const size_t tbl_bytes = size_t(4) * 32 * p.sigma * K * BW;
   constexpr int RS = ring_stride(L, NB);
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * RS;
-  uint8_t* okA = wbase + tbl_bytes + groups_alloc(L) * RS * 4 + size_t(g) * 2 * p.ring;
+  uint8_t* okA = wbase + tbl_bytes + groups_alloc(L) * RS * 4 + size_t(g) * ok_stride(p.ring);
   uint8_t* okB = okA + p.ring;
 
   const uint32_t lanes_real = p.W / R;          // host guarantees W % R == 0, lanes_real <= L

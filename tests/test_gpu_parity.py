@@ -226,3 +226,28 @@ def test_dense_u8_matches_u16():
         assert np.array_equal(ap.plot_dense_u8(x, y, c).astype(np.int32), gpu_grid(x, y, w, h, r))
     with pytest.raises(ap.ConfigError):
         ap.plot_dense_u8(x, y, cfg(128, 1, 1))
+
+
+@pytest.mark.parametrize("ndev", [2, 3, 4])
+def test_multi_device_row_shards(ndev, monkeypatch):
+    """The in-library multi-device path (contiguous row shards, x halo per shard,
+    count gather and in-order concatenation), with one GPU standing in for ndev
+    shard devices (AP_SHARDS_PER_DEVICE), equals the single-device result."""
+    monkeypatch.setenv("AP_SHARDS_PER_DEVICE", str(ndev))
+    rng = np.random.default_rng(40 + ndev)
+    x = rng.integers(1, 5, 900).astype(np.uint8)
+    y = np.concatenate([x[100:500], rng.integers(1, 5, 300)]).astype(np.uint8)
+    for w, h, r in ((48, 1, 1), (30, 3, 2)):
+        one = ap.plot_dense_u16(x, y, cfg(w, h, r, n_devices=1))
+        many = ap.plot_dense_u16(x, y, cfg(w, h, r, n_devices=ndev))
+        assert np.array_equal(one, many)
+        rc, want = ol.plot_rows(x, y, w, h, r)
+        assert np.array_equal(many.astype(np.int32), want)
+        t = int(np.quantile(want, 0.97))
+        r1 = ap.plot_threshold_arrays(x, y, cfg(w, h, r, n_devices=1), t)
+        rn = ap.plot_threshold_arrays(x, y, cfg(w, h, r, n_devices=ndev), t)
+        for a, b in zip(r1, rn):
+            assert np.array_equal(a, b)
+        # a row range split across shards
+        part = ap.plot_dense_u16(x, y, cfg(w, h, r, n_devices=ndev), 7, 7 + 2 * ndev + 5)
+        assert np.array_equal(part, one[7:7 + 2 * ndev + 5])
