@@ -1,0 +1,23 @@
+#!/usr/bin/env python3
+"""Small dense + threshold runs of every kernel family for compute-sanitizer (one tool per call)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_0909_2000_b200 import alignplot as ap  # noqa: E402
+
+rng = np.random.default_rng(3)
+x = rng.integers(1, 5, 300).astype(np.uint8)
+y = np.concatenate([x[20:200], rng.integers(1, 5, 150)]).astype(np.uint8)
+for w, h, r in ((40, 1, 1), (50, 2, 2), (64, 1, 2), (20, 3, 1)):
+    c = ap.PlotConfig(window_w=w, step_h=h, blowup_r=r, mode=ap.Mode.cuda)
+    g = ap.plot_dense_u16(x, y, c)
+    t = int(np.quantile(g, 0.9))
+    rr, cc, hh = ap.plot_threshold_arrays(x, y, c, t)
+    assert rr.size == int((g >= t).sum())
+xb = rng.integers(1, 61, 300).astype(np.uint8)   # large alphabet -> computed-mask kernel
+yb = rng.integers(1, 61, 400).astype(np.uint8)
+ap.plot_dense_u16(xb, yb, ap.PlotConfig(window_w=121, step_h=5, blowup_r=2, mode=ap.Mode.cuda))
+print("sanitize case ok")
