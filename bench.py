@@ -216,6 +216,7 @@ def run_engine(args, rank, world, local_rank):
     from paper_0909_2000_b200 import _native
     from paper_0909_2000_b200 import alignplot as ap
 
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     c, x, y = workload(args.config, world)
@@ -285,7 +286,8 @@ def run_engine(args, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_local = sum(step_ms) / 1000.0
     kern_local = sum(kern_ms) / len(kern_ms) / 1000.0
-    t = torch.tensor([t_local, kern_local], dtype=torch.float64, device=dev)
+    red_dev = dev if (world == 1 or dist.get_backend() == "nccl") else torch.device("cpu")
+    t = torch.tensor([t_local, kern_local], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max, kern_max = float(t[0]), float(t[1])
@@ -322,7 +324,7 @@ def run_engine(args, rank, world, local_rank):
     for _ in range(args.steps):
         e2e_step()
     t_e2e_local = time.perf_counter() - t0
-    te = torch.tensor([t_e2e_local], dtype=torch.float64, device=dev)
+    te = torch.tensor([t_e2e_local], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te[0])
@@ -343,7 +345,7 @@ def run_engine(args, rank, world, local_rank):
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_u8_step()
-        te8 = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        te8 = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te8, op=dist.ReduceOp.MAX)
         e2e_u8 = {"value": rows_global * cols * c.w * args.steps / float(te8[0]), "unit": "window-pair cell updates/s",
@@ -427,6 +429,8 @@ def main():
     ap_.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap_.add_argument("--ref-seconds", type=float, default=8.0, help="wall-clock budget of the CPU reference sample")
     ap_.add_argument("--no-cpu-baseline", action="store_true")
+    ap_.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                     help="gloo: exercise the N>1 code path with several ranks on one GPU (timing not meaningful)")
     args = ap_.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -435,7 +439,7 @@ def main():
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if args.impl == "engine":
+        if args.impl == "engine" and args.dist_backend == "nccl":
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
