@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -205,9 +206,18 @@ bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
 }  // namespace
 
 // ---- context ----------------------------------------------------------------
+// Launch plan for (W, w, r, sigma, dense): kernel shape, function, occupancy.
+struct LaunchPlan {
+  Shape sh;
+  bool spec = false;
+  apk::KernelFn fn = nullptr;
+  int per_sm = 0;
+};
+
 struct ap_ctx {
   int device = 0;
   int sms = 0;
+  std::map<uint64_t, LaunchPlan> plans;   // cached per (w, r, sigma, dense) and env overrides
   cudaStream_t stream = nullptr;
   cudaStream_t stream_copy = nullptr;   // D2H of finished row blocks (overlaps the comb kernel)
   cudaStream_t stream_b = nullptr;      // second compute stream: consecutive row blocks overlap
@@ -344,11 +354,35 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const uint32_t sent = sigma_y;
   const uint32_t sigma = sigma_y + (r == 2 ? 1 : 0);
 
-  Shape sh;
-  const bool spec = r == 2 && choose_shape2(w, sigma_y, dense, &sh);
-  if (!spec && !choose_shape(W, sigma, dense, &sh))
-    return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
-                sigma, W);
+  // launch plan (shape choice, function attributes, occupancy), cached per context;
+  // tuning overrides (AP_SHAPE, AP_SHAPE2, AP_NO_R2) bypass the cache
+  const bool overrides = std::getenv("AP_SHAPE") || std::getenv("AP_SHAPE2") || std::getenv("AP_NO_R2");
+  const uint64_t pkey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(sigma_y) << 2) | (dense ? 1 : 0);
+  LaunchPlan plan;
+  auto hit = overrides ? c->plans.end() : c->plans.find(pkey);
+  if (hit != c->plans.end()) {
+    plan = hit->second;
+  } else {
+    plan.spec = r == 2 && choose_shape2(w, sigma_y, dense, &plan.sh);
+    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh))
+      return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
+                  sigma, W);
+    plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense)
+                        : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm);
+    if (!plan.fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", plan.sh.L, plan.sh.R);
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.sh.smem)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&plan.per_sm, plan.fn, apk::kWarpsPerCta * 32,
+                                                     plan.sh.smem));
+    if (plan.per_sm < 1) return fail(AP_CONFIG, "kernel L=%d R=%d does not fit an SM", plan.sh.L, plan.sh.R);
+    if (!overrides) c->plans[pkey] = plan;
+  }
+  const Shape& sh = plan.sh;
+  const bool spec = plan.spec;
+  // the dynamic-smem limit is a per-function attribute and other plans may have
+  // lowered it since this plan was cached
+  CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem)));
 
   // code streams: the specialised r = 2 kernel reads raw y codes (the $ columns
   // are implicit); the generic kernel reads the $-interleaved stream
@@ -364,13 +398,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   CK(cudaGetLastError());
   c->last_launches += 3;
 
-  KernelFn fn = spec ? apk::pick_r2(sh.L, sh.R / 2, sh.K, dense) : pick_kernel(sh.L, sh.R, sh.K, dense, sh.xm);
-  if (!fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", sh.L, sh.R);
-  CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem)));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, apk::kWarpsPerCta * 32, sh.smem));
-  if (per_sm < 1) return fail(AP_CONFIG, "kernel L=%d R=%d does not fit an SM", sh.L, sh.R);
+  KernelFn fn = plan.fn;
+  const int per_sm = plan.per_sm;
   const size_t total_warps = size_t(c->sms) * per_sm * apk::kWarpsPerCta;
 
   // column segments: enough independent (strip pair, segment) tasks for ~4
