@@ -155,28 +155,31 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
 // W - count(K) is reported for K = 0 mod r and converted to half-units
 // (runner.cpp:31-35); dense mode stores it, threshold mode stages the hits
 // with their row-major rank (scoring.cpp:30-39).
-template <int L, int NB, bool DENSE>
-__device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_t* ringB, uint8_t* okA,
-                                              uint8_t* okB, uint32_t j, uint32_t g, uint32_t lane,
+template <int L, int NB, bool DENSE, bool CHECK>
+__device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t* ringB, uint8_t* ok,
+                                              uint32_t j, uint32_t g, uint32_t lane,
                                               int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
                                               uint32_t rA, uint32_t rB, bool hasA, bool hasB,
                                               uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
   const uint32_t rmask = p.ring - 1;
   const uint32_t rshift = p.r - 1;
+  const uint32_t dummy = 2 * p.ring;      // scratch byte in the group's padding
   constexpr int CPL = (NB + L - 1) / L;   // columns per lane (the last lane may get fewer real ones)
   const int32_t eb = E0 + int32_t(j) * CPL;
   uint32_t cmask = 0;   // bit 2c: strip A countable, bit 2c+1: strip B
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = e >= 0 && e < int32_t(nseg_cols) && (NB % L == 0 || j * CPL + c < NB);
+    const bool valid = (!CHECK || (e >= 0 && e < int32_t(nseg_cols))) && (NB % L == 0 || j * CPL + c < NB);
     const uint32_t k = ringB[j * CPL + c];
     const int32_t thr = e - kbase - int32_t(p.W);
     const int32_t kA = int32_t(k & 0xFFFFu), kB = int32_t(k >> 16);
     const bool cA = valid && kA > thr;
     const bool cB = valid && kB > thr;
-    if (cA) okA[uint32_t(kA + kbase) & rmask] = 1;
-    if (cB) okB[uint32_t(kB + kbase) & rmask] = 1;
+    // ok flags: byte 2*slot = strip A, 2*slot+1 = strip B; non-countable events
+    // write a dummy byte past the ring instead of branching
+    ok[cA ? ((uint32_t(kA + kbase) & rmask) << 1) : dummy] = 1;
+    ok[cB ? ((uint32_t(kB + kbase) & rmask) << 1) + 1 : dummy] = 1;
     cmask |= (uint32_t(cA) | (uint32_t(cB) << 1)) << (2 * c);
   }
   __syncwarp();
@@ -185,17 +188,19 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = e >= 0 && e < int32_t(nseg_cols) && (NB % L == 0 || j * CPL + c < NB);
-    uint32_t oA = 0, oB = 0;
-    if (valid) {
-      const uint32_t slot = uint32_t(e - int32_t(p.W)) & rmask;
-      oA = okA[slot];
-      oB = okB[slot];
-      okA[slot] = 0;
-      okB[slot] = 0;
+    const bool valid = (!CHECK || (e >= 0 && e < int32_t(nseg_cols))) && (NB % L == 0 || j * CPL + c < NB);
+    uint32_t o = 0;   // ok flags of slot K = e - W: bit 0 strip A, bit 8 strip B
+    if (!CHECK && NB % L == 0) {
+      uint16_t* o16 = reinterpret_cast<uint16_t*>(ok) + (uint32_t(e - int32_t(p.W)) & rmask);
+      o = *o16;
+      *o16 = 0;
+    } else if (valid) {
+      uint16_t* o16 = reinterpret_cast<uint16_t*>(ok) + (uint32_t(e - int32_t(p.W)) & rmask);
+      o = *o16;
+      *o16 = 0;
     }
-    const uint32_t cA = (cmask >> (2 * c)) & 1u, cB = (cmask >> (2 * c + 1)) & 1u;
-    acc += (cA + 1u - oA) | ((cB + 1u - oB) << 16);   // biased by +1 per half
+    const uint32_t cab = ((cmask >> (2 * c)) & 1u) | (((cmask >> (2 * c + 1)) & 1u) << 16);
+    acc += cab + 0x00010001u - ((o & 1u) | ((o & 0x100u) << 8));   // biased by +1 per half
     dl[c] = acc;
   }
   // exclusive scan of the lane totals across the group
@@ -212,10 +217,10 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = e >= 0 && e < int32_t(nseg_cols) && (NB % L == 0 || j * CPL + c < NB);
+    const bool valid = (!CHECK || (e >= 0 && e < int32_t(nseg_cols))) && (NB % L == 0 || j * CPL + c < NB);
     const uint32_t cnt = run + excl + dl[c] - bias0 - uint32_t(c + 1) * 0x00010001u;
     const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
-    const bool out_ok = valid && kp >= 0 && kp < int32_t(p.S) && !(uint32_t(kp) & rshift);
+    const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
     const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
     const int32_t llA = int32_t(p.W) - int32_t(cnt & 0xFFFFu);
     const int32_t llB = int32_t(p.W) - int32_t(cnt >> 16);
@@ -291,6 +296,24 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
   __syncwarp();
 }
 
+// Chunks whose bottom columns and window starts all lie inside the segment
+// (every chunk but the first few and the last) skip the per-column range checks.
+template <int L, int NB, bool DENSE>
+__device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_t* ringB, uint8_t* ok,
+                                              uint32_t j, uint32_t g, uint32_t lane,
+                                              int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
+                                              uint32_t rA, uint32_t rB, bool hasA, bool hasB,
+                                              uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
+  const bool interior = E0 >= int32_t(p.W) - 1 &&
+                        E0 + NB <= min(int32_t(nseg_cols), int32_t(p.S + p.W) - 1);
+  if (interior)
+    extract_body<L, NB, DENSE, false>(p, ringB, ok, j, g, lane, E0, nseg_cols, kbase, c0, rA, rB, hasA, hasB,
+                                      run, hitsA, hitsB);
+  else
+    extract_body<L, NB, DENSE, true>(p, ringB, ok, j, g, lane, E0, nseg_cols, kbase, c0, rA, rB, hasA, hasB,
+                                     run, hitsA, hitsB);
+}
+
 // Comb kernel (K2): fused $-interleave, seaweed combing, window extraction
 // and output for one (strip-pair group, column segment) task per warp.
 //
@@ -333,7 +356,6 @@ comb_kernel(const CombParams p) {
   uint4* tbl = reinterpret_cast<uint4*>(wbase);                       // [G][sigma][Q][L]
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + size_t(128) * p.sigma * R) + g * (kChunk + 1);
   uint8_t* okA = wbase + size_t(128) * p.sigma * R + G * (kChunk + 1) * 4 + size_t(g) * ok_stride(p.ring);
-  uint8_t* okB = okA + p.ring;
   const uint32_t rmask = p.ring - 1;
   const uint32_t rshift = p.r - 1;
   const uint32_t zero = p.zero;   // 0, opaque to ptxas so the HFMA2 is not folded into HMUL2
@@ -490,7 +512,7 @@ comb_kernel(const CombParams p) {
       ych2 = nxb;
       __syncwarp();
 
-      extract_chunk<L, kChunk, DENSE>(p, ringB, okA, okB, j, g, lane,
+      extract_chunk<L, kChunk, DENSE>(p, ringB, okA, j, g, lane,
                                       int32_t(ch * kChunk) - (VB - 1), nseg_cols, kbase, c0, rA, rB,
                                       hasA, hasB, run, hitsA, hitsB);
 
@@ -577,7 +599,6 @@ comb2_kernel(const CombParams p) {
   constexpr int RS = ring_stride(L, NB);
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * RS;
   uint8_t* okA = wbase + tbl_bytes + groups_alloc(L) * RS * 4 + size_t(g) * ok_stride(p.ring);
-  uint8_t* okB = okA + p.ring;
 
   const uint32_t lanes_real = p.W / R;          // host guarantees W % R == 0, lanes_real <= L
   const uint32_t VB = lanes_real * K;           // virtual bands down to the strip bottom
@@ -737,7 +758,7 @@ comb2_kernel(const CombParams p) {
       ych = nxa;
       ych2 = nxb;
       __syncwarp();
-      extract_chunk<L, NB, DENSE>(p, ringB, okA, okB, j, g, lane,
+      extract_chunk<L, NB, DENSE>(p, ringB, okA, j, g, lane,
                                   2 * (int32_t(ch * kChunk) - int32_t(VB - 1)), nseg_cols, kbase, c0, rA,
                                   rB, hasA, hasB, run, hitsA, hitsB);
       if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= kRebaseAt) {
