@@ -5,20 +5,27 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $(EXTRA_NVFLAGS)
 PKG := paper_0909_2000_b200
 CSRC := $(PKG)/csrc
-LIB := $(PKG)/libalignplot_b200.so
-OBJS := build/ap_capi.o build/ap_inst_l8.o build/ap_inst_l16.o build/ap_inst_l32.o build/ap_inst_r2.o
+BUILD ?= build
+LIB ?= $(PKG)/libalignplot_b200.so
+OBJS := $(BUILD)/ap_capi.o $(BUILD)/ap_inst_l8.o $(BUILD)/ap_inst_l16.o $(BUILD)/ap_inst_l32.o $(BUILD)/ap_inst_r2.o
 HDRS := $(CSRC)/ap_kernels.cuh $(CSRC)/ap_aux_kernels.cuh include/alignplot_b200.h
 
 all: $(LIB) oracle
 
-build/%.o: $(CSRC)/%.cu $(HDRS) | build
-	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+$(BUILD)/%.o: $(CSRC)/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; false)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
-build:
-	mkdir -p build
+$(BUILD):
+	mkdir -p $(BUILD)
+
+# experiment builds: make variant V=name FLAGS="-DFOO" -> tools/exp/name/libalignplot_b200.so
+# (load with AP_LIB_PATH=tools/exp/name/libalignplot_b200.so)
+variant:
+	$(MAKE) BUILD=tools/exp/$(V)/obj LIB=tools/exp/$(V)/libalignplot_b200.so EXTRA_NVFLAGS="$(FLAGS)" \
+	  tools/exp/$(V)/libalignplot_b200.so
 
 oracle:
 	$(MAKE) -C oracle
@@ -27,7 +34,7 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean variant
 
 # C++ drop-in test (reference test cases against alignplot_shim.hpp); runs on a GPU box.
 tests/cpp/test_shim: tests/cpp/test_shim.cpp $(CSRC)/alignplot_shim.hpp include/alignplot_b200.h $(LIB)

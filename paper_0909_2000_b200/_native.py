@@ -13,7 +13,8 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_size_t, c_uint16, c_uint32, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libalignplot_b200.so")
+# AP_LIB_PATH: load another build of the same engine (tuning experiments, tools/exp/)
+LIB_PATH = os.environ.get("AP_LIB_PATH") or os.path.join(_HERE, "libalignplot_b200.so")
 
 AP_OK, AP_CONFIG, AP_EMPTY, AP_INVALID, AP_CUDA, AP_NODEV, AP_CAPACITY, AP_NOMEM = range(8)
 AP_MAX_BLOWN_WINDOW = 1024

@@ -9,15 +9,21 @@ namespace apk {
 
 // K1: effective y code stream (fused $-interleave, scoring.cpp:5-17):
 // ycode[c] = r == 2 ? (c odd ? map[y[c/2]] : sent) : map[y[c]]; pad with 0.
+// With ycol != nullptr also the generic kernel's column words ycol[c] =
+// ycode[c] * 0x10001 followed by `total` zero words (what lanes j != 0 read).
 __global__ void ycode_kernel(const uint8_t* __restrict__ y, size_t n, uint32_t r, uint32_t sent,
                              const uint8_t* __restrict__ map, uint8_t* __restrict__ ycode,
-                             size_t total) {
+                             size_t total, uint32_t* __restrict__ ycol) {
   for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < total;
        c += size_t(gridDim.x) * blockDim.x) {
     const size_t N = n * r;
     uint8_t v = 0;
     if (c < N) v = (r == 2) ? ((c & 1) ? map[y[c >> 1]] : uint8_t(sent)) : map[y[c]];
     ycode[c] = v;
+    if (ycol) {
+      ycol[c] = uint32_t(v) * 0x00010001u;
+      ycol[total + c] = 0u;
+    }
   }
 }
 

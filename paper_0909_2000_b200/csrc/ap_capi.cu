@@ -90,7 +90,7 @@ struct Shape {
 // masks] + ~14 per-step overhead) + ~25 extraction ops, scaled up when fewer than
 // 16 warps per SM fit (registers from the compiled kernel, table in shared memory).
 bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
-  const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
+  const uint32_t ring = apk::ring_slots(W, apk::kChunk);
   // tuning override: AP_SHAPE="L,R,K[,xm]"
   if (const char* env = std::getenv("AP_SHAPE")) {
     int l = 0, r = 0, k = 0, xm = 0;
@@ -151,7 +151,7 @@ constexpr Shape2Def kShapes2[] = {
 bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
   if (std::getenv("AP_NO_R2")) return false;
   const uint32_t W = 2 * w;
-  const uint32_t ring = next_pow2(std::max<uint32_t>(128, W + 64));
+  const uint32_t ring = apk::ring_slots(W, 2 * apk::kChunk);
   // tuning override: AP_SHAPE2="L,RR,K"
   if (const char* env = std::getenv("AP_SHAPE2")) {
     int l = 0, rr = 0, k = 0;
@@ -228,7 +228,8 @@ struct ap_ctx {
   std::mutex mu;
   // scratch (grown on demand)
   uint8_t *d_x = nullptr, *d_y = nullptr, *d_xcode = nullptr, *d_ycode = nullptr, *d_map = nullptr;
-  size_t cap_x = 0, cap_y = 0, cap_xcode = 0, cap_ycode = 0;
+  size_t cap_x = 0, cap_y = 0, cap_xcode = 0, cap_ycode = 0, cap_ycol = 0;
+  uint32_t* d_ycol = nullptr;
   uint32_t* d_small = nullptr;   // [0] sigma, [1] zero flag
   uint32_t* h_small = nullptr;   // pinned mirror
   uint16_t* d_out = nullptr;
@@ -388,13 +389,14 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   // are implicit); the generic kernel reads the $-interleaved stream
   if ((rc = grow(&c->d_xcode, &c->cap_xcode, mx))) return rc;
   const size_t ylen = spec ? n : N;
-  const size_t ytot = ylen + 256;
+  const size_t ytot = (ylen + 256 + 31) / 32 * 32;
   if ((rc = grow(&c->d_ycode, &c->cap_ycode, ytot))) return rc;
   apk::xcode_kernel<<<std::min<size_t>((mx + 255) / 256, 4096), 256, 0, st>>>(d_x, mx, c->d_map,
                                                                                c->d_xcode);
   CK(cudaGetLastError());
+  if (!spec && (rc = grow(&c->d_ycol, &c->cap_ycol, 2 * ytot))) return rc;   // ytot: multiple of 32
   apk::ycode_kernel<<<std::min<size_t>((ytot + 255) / 256, 4096), 256, 0, st>>>(
-      d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot);
+      d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot, spec ? nullptr : c->d_ycol);
   CK(cudaGetLastError());
   c->last_launches += 3;
 
@@ -425,6 +427,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   apk::CombParams p{};
   p.xcode = c->d_xcode;
   p.ycode = c->d_ycode;
+  p.ycol = c->d_ycol;
+  p.ycol_zero = spec ? nullptr : c->d_ycol + ytot;
   p.rows = uint32_t(nrows);
   p.h = h;
   p.w = w;
@@ -461,7 +465,9 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     if ((rc = grow(&c->d_offs, &c->cap_offs, nrows * nseg + 1))) return rc;
     CK(cudaMemsetAsync(c->d_segc + nrows * nseg, 0, sizeof(uint32_t), st));
     CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
-    p.t_half = cfg->threshold_half;
+    // the kernel tests h >= t in biased 16-bit halves: |h| <= 2048, so clamping t
+    // to +-0x4000 keeps every comparison exact
+    p.t_half = std::min<int32_t>(0x4000, std::max<int32_t>(-0x4000, cfg->threshold_half));
     p.stage = c->d_stage;
     p.cursor = c->d_cursor;
     p.stage_cap = c->cap_stage;
@@ -626,7 +632,7 @@ int ap_ctx_destroy(ap_ctx* c) {
   }
   DevGuard dg(c->device);
   cudaStreamSynchronize(c->stream);
-  for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_map,
+  for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_ycol, (void*)c->d_map,
                   (void*)c->d_small, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
                   (void*)c->d_segc, (void*)c->d_offs, c->d_cub, (void*)c->d_orow, (void*)c->d_ocol,
                   (void*)c->d_ohalf})

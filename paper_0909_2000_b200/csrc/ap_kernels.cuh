@@ -53,6 +53,8 @@ constexpr uint32_t kRebaseBy = 0x4000u;
 struct CombParams {
   const uint8_t* xcode;   // mapped x codes (0xFF = absent from y), local row 0 at xcode[0]
   const uint8_t* ycode;   // effective y codes, N entries + >=128 pad bytes, 16-B aligned
+  const uint32_t* ycol;   // generic kernel: code * ycol_mult per effective column (+256 pad), 16-B aligned
+  const uint32_t* ycol_zero;  // as many zero words (the column words seen by lanes j != 0)
   uint32_t rows;          // grid rows in this launch
   uint32_t h, w, r, W, N; // step, window, blowup, blown window, effective y length
   uint32_t sigma;         // table codes (incl. the sentinel code when r = 2)
@@ -97,9 +99,18 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __host__ __device__ constexpr int groups_per_warp(int L) { return 32 / L; }
 __host__ __device__ constexpr int groups_alloc(int L) { return 32 / L + (32 % L ? 1 : 0); }
 __host__ __device__ constexpr int ring_stride(int L, int nb) { return L * ((nb + L - 1) / L) + 1; }
-// ok-flag bytes per group: two rings (strips A, B) plus 32 bytes of padding so
-// the same slot of different groups falls in different banks (8 banks apart).
-__host__ __device__ constexpr size_t ok_stride(uint32_t ring) { return size_t(2) * ring + 32; }
+// ok-flag bytes per group: one u32 per ring slot (byte 0 = strip A, byte 2 =
+// strip B, so a slot reads back as the packed pair oA | oB << 16) plus 32 bytes
+// of padding so the same slot of different groups falls 8 banks apart.
+__host__ __device__ constexpr size_t ok_stride(uint32_t ring) { return size_t(4) * ring + 32; }
+// ring slots the extraction needs: the W + NB starts between the oldest unread
+// flag and the newest bottom column, plus the clear-ahead window of NB + 31
+// (extract_body); a power of two
+__host__ __device__ constexpr uint32_t ring_slots(uint32_t W, int nb) {
+  uint32_t need = W + 2 * uint32_t(nb) + 31, r = 128;
+  while (r < need) r <<= 1;
+  return r;
+}
 
 template <int L>
 __device__ __forceinline__ uint32_t shfl_up1(uint32_t v) {
@@ -116,6 +127,71 @@ template <int L>
 __device__ __forceinline__ uint32_t shfl_group_last(uint32_t v, uint32_t g) {
   if constexpr ((L & (L - 1)) == 0) return __shfl_sync(0xFFFFFFFFu, v, L - 1, L);
   else return __shfl_sync(0xFFFFFFFFu, v, (g * L + L - 1) & 31u);
+}
+
+// 16-byte shared load at a 32-bit shared-window address
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+#ifndef AP_KH
+#define AP_KH 0
+#endif
+#ifndef AP_YUNI
+#define AP_YUNI 0
+#endif
+#ifndef AP_R2_MB4
+#define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
+#endif
+
+// shared-window accesses by 32-bit address (ok-flag slots)
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_zero_v2(uint32_t addr) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %1};" :: "r"(addr), "r"(0u) : "memory");
+}
+__device__ __forceinline__ void sts_zero_v4(uint32_t addr) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" :: "r"(addr), "r"(0u) : "memory");
+}
+
+// hi32(a * b) + c on the FMA pipe
+__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// fp16x2 inequality as 1.0 / 0.0 per half (HSET2.BF); codes compared as fp16 bit
+// patterns (0..0x1FF, never NaN, no FTZ for f16: tools/int_peak.cu set_ne check)
+__device__ __forceinline__ uint32_t hset2_ne(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("set.ne.f16x2.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// fp16x2 product (keys are positive finite fp16 patterns: k * 1.0 = k, k * 0 = +0)
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// a * b + c on the FMA pipe (b opaque to ptxas so it cannot become an IADD)
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
 
 __device__ __forceinline__ uint32_t lop3_xor(uint32_t a, uint32_t b, uint32_t c) {
@@ -139,8 +215,9 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
                                                      int nb = kChunk) {
   const int Ga = groups_alloc(L);
   const size_t bytes = size_t(4) * 32 * sigma * table_words   // mismatch table (sigma = 0: computed masks)
-       + size_t(Ga) * ring_stride(L, nb) * 4                   // bottom-key ring per group (padded)
-       + size_t(Ga) * ok_stride(ring);                         // ok flags per group (strip A, strip B)
+       + ((size_t(Ga) * ring_stride(L, nb) * 4 + 15) & ~size_t(15))   // bottom-key ring per group (padded)
+       + size_t(32 / L) * ok_stride(ring)                      // ok flags per group (strip A, strip B)
+       + (Ga > 32 / L ? 64 : 0);                               // phantom group: ring mask 0, 64-B scratch
   return (bytes + 15) & ~size_t(15);                           // keep every warp's table 16-B aligned
 }
 
@@ -153,88 +230,124 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
 // (the heap of seaweed_scalar.cpp:80-97 replaced by a difference recurrence,
 // DESIGN.md §4), evaluated as a segmented scan over the group.  LLCS(K) =
 // W - count(K) is reported for K = 0 mod r and converted to half-units
-// (runner.cpp:31-35); dense mode stores it, threshold mode stages the hits
-// with their row-major rank (scoring.cpp:30-39).
+// (runner.cpp:31-35, scoring.cpp:26-28).
+//
+// Both strips are handled in packed 16-bit halves throughout:
+//  * kk = min_u16(k - thr - 1, C) (one VIADDMNMX): countable seaweeds give
+//    0..W-1 (= start - (e - W + 1)), the rest wrap to >= 0x8000 and clamp to
+//    C = 0x8000 | (W - 1 + A); bit 15 of kk is then "not countable" and
+//    (kk + e - W + 1) mod ring is the flag slot -- for non-countable seaweeds
+//    the slot of start e + A, a start whose flag nobody has written yet.
+//  * Clear-ahead: each chunk zeroes the slots of starts [E0 + A, E0 + A + NB)
+//    (A = NB + (-E0 mod 32): 32-aligned, so whole lane runs are vector stores).
+//    Those starts cannot have exited yet (A >= NB), so the stray flags of the
+//    chunk (all aimed inside this range) are wiped before the slot is used,
+//    and no per-seaweed select or branch is needed.  Live slots span
+//    W + NB + A <= W + 2 NB + 31 starts (ring_slots).
+//  * Slot addresses and the running count use IMAD / IMAD.HI on the FMA pipe.
+// Packed 32-bit sums are exact whenever every half of the final value is in
+// [0, 0xFFFF] (arithmetic is linear mod 2^32), so no per-column bias is needed.
 template <int L, int NB, bool DENSE, bool CHECK>
-__device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t* ringB, uint8_t* ok,
-                                              uint32_t j, uint32_t g, uint32_t lane,
+__device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t* ringB, uint32_t okb,
+                                              uint32_t rmask, uint32_t j, uint32_t g, uint32_t lane,
                                               int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
                                               uint32_t rA, uint32_t rB, bool hasA, bool hasB,
                                               uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
-  const uint32_t rmask = p.ring - 1;
-  const uint32_t rshift = p.r - 1;
-  const uint32_t dummy = 2 * p.ring;      // scratch byte in the group's padding
   constexpr int CPL = (NB + L - 1) / L;   // columns per lane (the last lane may get fewer real ones)
+  const uint32_t rshift = p.r - 1;
+  const uint32_t one = p.one;
   const int32_t eb = E0 + int32_t(j) * CPL;
-  uint32_t cmask = 0;   // bit 2c: strip A countable, bit 2c+1: strip B
+  const uint32_t A = NB + (uint32_t(-E0) & 31u);                    // E0 mod 32 is the same every chunk
+  const uint32_t clamp2 = (0x8000u | (p.W - 1 + A)) * 0x00010001u;
+  const uint32_t rmask2 = rmask * 0x00010001u;
+  const uint32_t n0 = (uint32_t(kbase + int32_t(p.W) - 1 - eb) & 0xFFFFu) * 0x00010001u;   // -(thr+1) at eb
+  const uint32_t sb2 = (uint32_t(eb - int32_t(p.W) + 1) & rmask) * 0x00010001u;            // slot of start eb-W+1
+  const uint32_t xA = okb * 0x00010001u + 0x20000u;   // addrA = imad(addrB, -65536, imad(slot2, 4, xA))
+
+  // ---- phase 1: scatter the ok flags of countable seaweeds
+  uint32_t nc[CPL];   // bit 15 / 31: column not countable (strip A / B)
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = (!CHECK || (e >= 0 && e < int32_t(nseg_cols))) && (NB % L == 0 || j * CPL + c < NB);
-    const uint32_t k = ringB[j * CPL + c];
-    const int32_t thr = e - kbase - int32_t(p.W);
-    const int32_t kA = int32_t(k & 0xFFFFu), kB = int32_t(k >> 16);
-    const bool cA = valid && kA > thr;
-    const bool cB = valid && kB > thr;
-    // ok flags: byte 2*slot = strip A, 2*slot+1 = strip B; non-countable events
-    // write a dummy byte past the ring instead of branching
-    ok[cA ? ((uint32_t(kA + kbase) & rmask) << 1) : dummy] = 1;
-    ok[cB ? ((uint32_t(kB + kbase) & rmask) << 1) + 1 : dummy] = 1;
-    cmask |= (uint32_t(cA) | (uint32_t(cB) << 1)) << (2 * c);
+    const bool real = NB % L == 0 || j * CPL + c < NB;
+    const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
+    const uint32_t k = real ? ringB[j * CPL + c] : 0u;
+    const uint32_t negc = ((0x10000u - uint32_t(c)) & 0xFFFFu) * 0x00010001u;
+    const uint32_t nthr = c == 0 ? n0 : __vadd2(n0, negc);
+    uint32_t kk = __viaddmin_u16x2(k, nthr, clamp2);
+    if (!valid) kk = clamp2;
+    const uint32_t pre = kk + sb2 + uint32_t(c) * 0x00010001u;   // halves < 0x10000: no carry
+    const uint32_t slot2 = pre & rmask2;
+    nc[c] = pre & 0x80008000u;
+    const uint32_t addrB = madhi(slot2, 1u << 18, okb + 2);     // okb + 4 * slotB + 2
+    const uint32_t addrA = imad(addrB, 0xFFFF0000u, imad(slot2, 4u, xA));   // okb + 4 * slotA
+    sts_u8(addrA, 1u);
+    sts_u8(addrB, 1u);
   }
   __syncwarp();
-  uint32_t dl[CPL];
+
+  // ---- phase 2: read the flags of starts e - W; acc = sum(not countable + ok)
+  const uint32_t rsb = uint32_t(eb - int32_t(p.W)) & rmask;
   uint32_t acc = 0;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
-    const bool valid = (!CHECK || (e >= 0 && e < int32_t(nseg_cols))) && (NB % L == 0 || j * CPL + c < NB);
-    uint32_t o = 0;   // ok flags of slot K = e - W: bit 0 strip A, bit 8 strip B
-    if (!CHECK && NB % L == 0) {
-      uint16_t* o16 = reinterpret_cast<uint16_t*>(ok) + (uint32_t(e - int32_t(p.W)) & rmask);
-      o = *o16;
-      *o16 = 0;
-    } else if (valid) {
-      uint16_t* o16 = reinterpret_cast<uint16_t*>(ok) + (uint32_t(e - int32_t(p.W)) & rmask);
-      o = *o16;
-      *o16 = 0;
-    }
-    const uint32_t cab = ((cmask >> (2 * c)) & 1u) | (((cmask >> (2 * c + 1)) & 1u) << 16);
-    acc += cab + 0x00010001u - ((o & 1u) | ((o & 0x100u) << 8));   // biased by +1 per half
-    dl[c] = acc;
+    const bool real = NB % L == 0 || j * CPL + c < NB;
+    const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
+    uint32_t o = 0;
+    if ((!CHECK && NB % L == 0) || valid) o = lds_u32(okb + 4 * ((rsb + c) & rmask));
+    acc = imad(o, one, madhi(nc[c], 1u << 17, acc));   // acc + (nc >> 15) + o
+    nc[c] = acc;                                         // running sum after column c
   }
-  // exclusive scan of the lane totals across the group
-  uint32_t incl = acc;
+  // clear ahead: starts [E0 + A, E0 + A + NB), this lane's run of CPL
+  {
+    const uint32_t cb = uint32_t(E0 + int32_t(A) + int32_t(j) * CPL) & rmask;
+    if constexpr (NB % L == 0 && (CPL == 4 || CPL == 8 || CPL == 16)) {
+#pragma unroll
+      for (int q = 0; q < CPL / 4; ++q) sts_zero_v4(okb + 4 * cb + 16 * q);
+    } else if constexpr (NB % L == 0 && CPL == 2) {
+      sts_zero_v2(okb + 4 * cb);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        if (NB % L == 0 || j * CPL + c < NB) sts_u32(okb + 4 * ((cb + c) & rmask), 0u);
+    }
+  }
+  // lane total of count deltas (1 - nc - o per real column; invalid columns add 0)
+  const uint32_t tot = uint32_t(CPL) * 0x00010001u - acc;
+  uint32_t incl = tot;
 #pragma unroll
   for (int off = 1; off < L; off <<= 1) {
     const uint32_t v = shfl_up_n<L>(incl, off);
     if (j >= uint32_t(off)) incl += v;
   }
-  const uint32_t excl = incl - acc;
-  const uint32_t bias0 = j * CPL * 0x00010001u;
-  uint32_t hmA = 0, hmB = 0;      // threshold hits of this lane's columns (bit c)
-  uint32_t hv[DENSE ? 1 : CPL];   // packed half-unit scores hA | hB << 16
+  // count after column c = runc + c * 0x10001 - sum_c;  half = Kh - 2 * count
+  const uint32_t runc = run + incl - tot + 0x00010001u;
+  run = shfl_group_last<L>(run + incl, g);
+  const uint32_t kh = (2 * p.W - (rshift ? 2 * p.w : 0u)) * 0x00010001u;
+  if constexpr (DENSE) {
+    // packed halves biased by 0x8000 (r = 2 scores can be negative)
+    const uint32_t kb = imad(runc, 0xFFFFFFFEu, kh + 0x80008000u);
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    const int32_t e = eb + c;
-    const bool valid = (!CHECK || (e >= 0 && e < int32_t(nseg_cols))) && (NB % L == 0 || j * CPL + c < NB);
-    const uint32_t cnt = run + excl + dl[c] - bias0 - uint32_t(c + 1) * 0x00010001u;
-    const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
-    const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
-    const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
-    const int32_t llA = int32_t(p.W) - int32_t(cnt & 0xFFFFu);
-    const int32_t llB = int32_t(p.W) - int32_t(cnt >> 16);
-    const int32_t hA = 2 * llA - (rshift ? 2 * int32_t(p.w) : 0);
-    const int32_t hB = 2 * llB - (rshift ? 2 * int32_t(p.w) : 0);
-    if constexpr (DENSE) {
+    for (int c = 0; c < CPL; ++c) {
+      const int32_t e = eb + c;
+      const bool real = NB % L == 0 || j * CPL + c < NB;
+      const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
+      const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
+      const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
+      const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
+      const uint32_t hb = imad(nc[c], 2u, kb - uint32_t(2 * c) * 0x00010001u);   // (h + 0x8000) per half
+      const uint32_t hlo = hb - 0x8000u;                       // low 16 bits: hA
+      const uint32_t hhi = madhi(hb, 0x10000u, 0xFFFF8000u);   // low 16 bits: hB
       if (p.out_kind == 0) {
-        if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hA);
-        if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hB);
+        if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hlo);
+        if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hhi);
       } else if (p.out_kind == 2) {   // compact: half-units as bytes (w <= 127)
-        if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(hA);
-        if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(hB);
+        if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(hlo);
+        if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(hhi);
       } else {
         // write_pgm (io.cpp:136-153): pixel = (255*clamp(h,0,2w) + w) / 2w, cut -> 0
+        const int32_t hA = int32_t(int16_t(uint16_t(hlo))), hB = int32_t(int16_t(uint16_t(hhi)));
         const int32_t full = 2 * int32_t(p.w);
         const bool cutA = p.has_pgm_threshold && hA < p.pgm_threshold;
         const bool cutB = p.has_pgm_threshold && hB < p.pgm_threshold;
@@ -243,16 +356,28 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
         if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(qA);
         if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(qB);
       }
-    } else {
-      hmA |= uint32_t(out_ok && hasA && hA >= p.t_half) << c;
-      hmB |= uint32_t(out_ok && hasB && hB >= p.t_half) << c;
-      hv[c] = uint32_t(hA) | (uint32_t(hB) << 16);
     }
-  }
-  if constexpr (!DENSE) {
+  } else {
+    // (h + 0x8000 - t) per half: bit 15 set iff h >= t (t clamped to +-0x4000 by the host)
+    const uint32_t kt = imad(runc, 0xFFFFFFFEu, kh + (0x8000u - uint32_t(p.t_half)) * 0x00010001u);
+    uint32_t any = 0;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) any |= imad(nc[c], 2u, kt - uint32_t(2 * c) * 0x00010001u);
     // Row-major ranks: a hit's rank in its (row, segment) = the row's earlier
     // hits (previous chunks, lower lanes of this chunk, lower columns of this lane).
-    if (__any_sync(0xFFFFFFFFu, hmA | hmB)) {
+    if (__any_sync(0xFFFFFFFFu, any & 0x80008000u)) {
+      uint32_t hmA = 0, hmB = 0;   // threshold hits of this lane's columns (bit c)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int32_t e = eb + c;
+        const bool real = NB % L == 0 || j * CPL + c < NB;
+        const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
+        const int32_t kp = e - int32_t(p.W) + 1;
+        const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
+        const uint32_t ht = imad(nc[c], 2u, kt - uint32_t(2 * c) * 0x00010001u);
+        hmA |= uint32_t(out_ok && hasA && (ht & 0x8000u)) << c;
+        hmB |= uint32_t(out_ok && hasB && (ht & 0x80000000u)) << c;
+      }
       const uint32_t nA = __popc(hmA), nB = __popc(hmB);
       const uint32_t pk = nA | (nB << 16);
       uint32_t gi = pk;
@@ -274,16 +399,19 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
       if (lane == 0) pos = atomicAdd(p.cursor, (unsigned long long)wtot);
       pos = __shfl_sync(0xFFFFFFFFu, pos, 0) + (wi - nA - nB);
       uint32_t rkA = hitsA + (gex & 0xFFFFu), rkB = hitsB + (gex >> 16);
+      const uint32_t kb = imad(runc, 0xFFFFFFFEu, kh + 0x80008000u);
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const uint32_t gcol = (c0 + uint32_t(eb + c - int32_t(p.W) + 1)) >> rshift;
+        const uint32_t hb = imad(nc[c], 2u, kb - uint32_t(2 * c) * 0x00010001u);
+        const uint32_t hA = uint32_t(int32_t(hb & 0xFFFFu) - 0x8000), hB = uint32_t(int32_t(hb >> 16) - 0x8000);
         if ((hmA >> c) & 1u) {
-          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hv[c] & 0xFFFFu, rkA);
+          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hA & 0xFFFFu, rkA);
           ++pos;
           ++rkA;
         }
         if ((hmB >> c) & 1u) {
-          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hv[c] >> 16, rkB);
+          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hB & 0xFFFFu, rkB);
           ++pos;
           ++rkB;
         }
@@ -292,14 +420,13 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
       hitsB += gtot >> 16;
     }
   }
-  run = shfl_group_last<L>(run + incl - (j + 1) * CPL * 0x00010001u, g);
-  __syncwarp();
 }
 
 // Chunks whose bottom columns and window starts all lie inside the segment
 // (every chunk but the first few and the last) skip the per-column range checks.
 template <int L, int NB, bool DENSE>
-__device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_t* ringB, uint8_t* ok,
+__device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_t* ringB, uint32_t okb,
+                                              uint32_t rmask,
                                               uint32_t j, uint32_t g, uint32_t lane,
                                               int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
                                               uint32_t rA, uint32_t rB, bool hasA, bool hasB,
@@ -307,10 +434,10 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
   const bool interior = E0 >= int32_t(p.W) - 1 &&
                         E0 + NB <= min(int32_t(nseg_cols), int32_t(p.S + p.W) - 1);
   if (interior)
-    extract_body<L, NB, DENSE, false>(p, ringB, ok, j, g, lane, E0, nseg_cols, kbase, c0, rA, rB, hasA, hasB,
+    extract_body<L, NB, DENSE, false>(p, ringB, okb, rmask, j, g, lane, E0, nseg_cols, kbase, c0, rA, rB, hasA, hasB,
                                       run, hitsA, hitsB);
   else
-    extract_body<L, NB, DENSE, true>(p, ringB, ok, j, g, lane, E0, nseg_cols, kbase, c0, rA, rB, hasA, hasB,
+    extract_body<L, NB, DENSE, true>(p, ringB, okb, rmask, j, g, lane, E0, nseg_cols, kbase, c0, rA, rB, hasA, hasB,
                                      run, hitsA, hitsB);
 }
 
@@ -345,6 +472,10 @@ comb_kernel(const CombParams p) {
   constexpr int RB = R / K;       // rows per band
   constexpr int QB = RB / 4;      // quads per band
   constexpr int VB = L * K;       // virtual bands per strip (wavefront depth)
+  // the last KH bands compute their masks on the fp16 pipe (HSET2 + HMUL2) instead
+  // of reading the table: fewer shared-memory wavefronts per cell
+  constexpr int KH = XM ? 0 : (AP_KH < K ? AP_KH : K - 1);
+  constexpr uint32_t kTblMul = uint32_t(Q * L * 16) << 16;   // (code * 0x10001) -> code * table stride
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
@@ -355,10 +486,9 @@ comb_kernel(const CombParams p) {
   unsigned char* wbase = smem + warp * per_warp;
   uint4* tbl = reinterpret_cast<uint4*>(wbase);                       // [G][sigma][Q][L]
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + size_t(128) * p.sigma * R) + g * (kChunk + 1);
-  uint8_t* okA = wbase + size_t(128) * p.sigma * R + G * (kChunk + 1) * 4 + size_t(g) * ok_stride(p.ring);
-  const uint32_t rmask = p.ring - 1;
+  const uint32_t okb = uint32_t(__cvta_generic_to_shared(wbase + size_t(128) * p.sigma * R)) +
+                       ((G * (kChunk + 1) * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
   const uint32_t rshift = p.r - 1;
-  const uint32_t zero = p.zero;   // 0, opaque to ptxas so the HFMA2 is not folded into HMUL2
 
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + G - 1) / G;
@@ -379,6 +509,7 @@ comb_kernel(const CombParams p) {
     // ---- mismatch table / x-code registers (fused $-interleave, scoring.cpp:5-17)
     __syncwarp();
     uint32_t xpair[XM ? R : 1];
+    uint32_t xh[KH > 0 ? KH * RB : 1];   // x code pairs of the computed-mask bands (fp16 patterns)
     {
       uint32_t xa[R], xb[R];
 #pragma unroll
@@ -404,6 +535,8 @@ comb_kernel(const CombParams p) {
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) xpair[rho] = xa[rho] | (xb[rho] << 16);
       } else {
+#pragma unroll
+        for (int i = 0; i < KH * RB; ++i) xh[i] = xa[(K - KH) * RB + i] | (xb[(K - KH) * RB + i] << 16);
         uint4* tg = tbl + size_t(g) * p.sigma * Q * L;
         for (uint32_t a = 0; a < p.sigma; ++a) {
 #pragma unroll
@@ -418,39 +551,51 @@ comb_kernel(const CombParams p) {
           }
         }
       }
-      for (uint32_t k = j; k < 2 * p.ring; k += L) okA[k] = 0;
+      for (uint32_t k = j; k < p.ring; k += L) sts_u32(okb + 4 * k, 0u);
     }
     __syncwarp();
 
-    const uint4* tl = tbl + size_t(g) * p.sigma * Q * L + j;
-    const uint64_t* yw = reinterpret_cast<const uint64_t*>(p.ycode + c0);
+    // table base of this lane; y column words are byte offsets of a code's quads
+    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + size_t(g) * p.sigma * Q * L + j));
+#if AP_YUNI
+    const uint4* yq = reinterpret_cast<const uint4*>(p.ycol + c0);   // warp-uniform loads
+    const uint32_t zj = j == 0 ? 1u : 0u;
+#else
+    const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
+#endif
+    // lane-select constants: the band-0 inputs are imad(shuffled, nz, own) on the
+    // FMA pipe instead of selects (own = fresh key / new column word on lane 0, 0 elsewhere)
+    const uint32_t nz = j != 0 ? 1u : 0u;
+    const uint32_t finc = j == 0 ? 0x00010001u : 0u;
 
     uint32_t V[R];
 #pragma unroll
     for (int rho = 0; rho < R; ++rho) V[rho] = 0u;     // left-boundary seaweeds: key 0
     uint32_t tb[K];     // seaweed leaving band b at the previous step
-    uint32_t cd[K];     // y code of band b at the current step
+    uint32_t cd[K];     // y column word of band b at the current step
 #pragma unroll
     for (int b = 0; b < K; ++b) { tb[b] = 0u; cd[b] = 0u; }
     int32_t kbase = -int32_t(p.W) - 1;                 // key(c) = c - kbase > W for top seaweeds
-    uint32_t fresh = uint32_t(-kbase) * 0x00010001u;   // key of column s, both halves
+    uint32_t fresh = j == 0 ? uint32_t(-kbase) * 0x00010001u : 0u;   // key of column s, both halves
+    const uint32_t one = p.one;
+    const uint32_t tblmul = kTblMul * one;   // opaque: keeps IMAD.HI (FMA pipe), not LEA.HI (ALU)
     uint32_t run = 0u;
     uint32_t hitsA = 0u, hitsB = 0u;
 
-    // lane 0's y codes: one 32-byte chunk of the code stream per 32 steps, prefetched
-    uint4 ych = __ldg(reinterpret_cast<const uint4*>(yw));
-    uint4 ych2 = __ldg(reinterpret_cast<const uint4*>(yw) + 1);
-    if (j == 0) cd[0] = ych.x & 0xFFu;                 // column 0
+    // group lane 0's y words: a queue of the next 16 columns, refilled 8 at a time
+    // (register moves and IMADs only: no byte extraction on the ALU pipe)
+    uint4 qa = __ldg(yq), qb = __ldg(yq + 1), qc = __ldg(yq + 2), qd = __ldg(yq + 3);
+#if AP_YUNI
+    cd[0] = qa.x * zj;
+#else
+    cd[0] = qa.x;                                      // column 0 (0 on lanes j != 0)
+#endif
+    uint32_t nsub = 0;
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
-      const uint4 nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
-      const uint4 nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
 #pragma unroll 1
-      for (int sub = 0; sub < kChunk / 8; ++sub) {
-        // lane 0's codes for steps sub*8+1 .. sub*8+8 (the last from the next chunk)
-        const uint32_t w0 = sub == 0 ? ych.x : sub == 1 ? ych.z : sub == 2 ? ych2.x : ych2.z;
-        const uint32_t w1 = sub == 0 ? ych.y : sub == 1 ? ych.w : sub == 2 ? ych2.y : ych2.w;
-        const uint32_t w2 = sub == 0 ? ych.z : sub == 1 ? ych2.x : sub == 2 ? ych2.z : nxa.x;
+      for (int sub = 0; sub < kChunk / 8; ++sub, ++nsub) {
+        const uint4 na = __ldg(yq + 2 * nsub + 4), nb = __ldg(yq + 2 * nsub + 5);
         uint32_t* ring_sub = ringB + sub * 8;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -458,23 +603,36 @@ comb_kernel(const CombParams p) {
           uint4 nfq[Q];
           if constexpr (!XM) {
 #pragma unroll
-            for (int b = 0; b < K; ++b)
+            for (int b = 0; b < K - KH; ++b)
 #pragma unroll
-              for (int qq = 0; qq < QB; ++qq) nfq[b * QB + qq] = tl[(cd[b] * Q + b * QB + qq) * L];
+              for (int qq = 0; qq < QB; ++qq)
+                nfq[b * QB + qq] = lds128(madhi(cd[b], tblmul, tlb) + (b * QB + qq) * L * 16);
           }
           // seaweeds entering each band
           uint32_t tin[K];
           {
             const uint32_t sh = shfl_up1<L>(tb[K - 1]);
-            tin[0] = j == 0 ? fresh : sh;
+            tin[0] = imad(sh, nz, fresh);
 #pragma unroll
             for (int b = 1; b < K; ++b) tin[b] = tb[b - 1];
           }
-          fresh += 0x00010001u;
+          fresh = imad(fresh, one, finc);
 #pragma unroll
           for (int b = 0; b < K; ++b) {
             uint32_t t = tin[b];
-            const uint32_t yrep = cd[b] * 0x00010001u;
+            const uint32_t yrep = cd[b];                 // code * 0x10001
+            if (!XM && b >= K - KH) {
+#pragma unroll
+              for (int k = 0; k < RB; ++k) {
+                uint32_t& v = V[b * RB + k];
+                const uint32_t mm = hset2_ne(xh[(b - (K - KH)) * RB + k], yrep);   // 1.0 where codes differ
+                const uint32_t d = __vmaxu2(hmul2(t, mm), v);                      // match: max(0, V) = V
+                v = lop3_xor(v, t, d);
+                t = d;
+              }
+              tb[b] = t;
+              continue;
+            }
 #pragma unroll
             for (int qq = 0; qq < QB; ++qq) {
               uint32_t m[4];
@@ -499,20 +657,23 @@ comb_kernel(const CombParams p) {
           if (j == L - 1) ring_sub[u] = tb[K - 1];
           // codes of the next step: band b takes band b-1's, band 0 lane j-1's last band's
           {
-            const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
-            const uint32_t ynew = (ww >> (8 * ((u + 1) & 3))) & 0xFFu;
+            const uint32_t ynew = u == 0 ? qa.y : u == 1 ? qa.z : u == 2 ? qa.w : u == 3 ? qb.x :
+                                  u == 4 ? qb.y : u == 5 ? qb.z : u == 6 ? qb.w : qc.x;
             const uint32_t sh = shfl_up1<L>(cd[K - 1]);
 #pragma unroll
             for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
-            cd[0] = j == 0 ? ynew : sh;
+#if AP_YUNI
+            cd[0] = imad(sh, nz, imad(ynew, zj, 0u));
+#else
+            cd[0] = imad(sh, nz, ynew);
+#endif
           }
         }
+        qa = qc; qb = qd; qc = na; qd = nb;
       }
-      ych = nxa;
-      ych2 = nxb;
       __syncwarp();
 
-      extract_chunk<L, kChunk, DENSE>(p, ringB, okA, j, g, lane,
+      extract_chunk<L, kChunk, DENSE>(p, ringB, okb, p.ring - 1, j, g, lane,
                                       int32_t(ch * kChunk) - (VB - 1), nseg_cols, kbase, c0, rA, rB,
                                       hasA, hasB, run, hitsA, hitsB);
 
@@ -523,7 +684,7 @@ comb_kernel(const CombParams p) {
         for (int rho = 0; rho < R; ++rho) V[rho] = __vmaxu2(V[rho], by) - by;
 #pragma unroll
         for (int b = 0; b < K; ++b) tb[b] = __vmaxu2(tb[b], by) - by;
-        fresh -= by;
+        if (j == 0) fresh -= by;
         kbase += int32_t(kRebaseBy);
       }
     }
@@ -575,7 +736,7 @@ __device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t*
 }
 
 template <int L, int RR, int K, bool DENSE>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= 8 ? 4 : (RR <= 16 ? 3 : 2))
+__global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= AP_R2_MB4 ? 4 : (RR <= 16 ? 3 : 2))
 comb2_kernel(const CombParams p) {
   static_assert(L <= 32 && RR % K == 0, "bad shape");
   constexpr int G = groups_per_warp(L);     // real groups; lanes >= G*L are idle
@@ -598,7 +759,10 @@ comb2_kernel(const CombParams p) {
   const size_t tbl_bytes = size_t(4) * 32 * p.sigma * K * BW;
   constexpr int RS = ring_stride(L, NB);
   uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbl_bytes) + g * RS;
-  uint8_t* okA = wbase + tbl_bytes + groups_alloc(L) * RS * 4 + size_t(g) * ok_stride(p.ring);
+  const uint32_t okb = uint32_t(__cvta_generic_to_shared(wbase + tbl_bytes)) +
+                       ((groups_alloc(L) * RS * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
+  // the phantom group (lanes >= G*L) folds every ok slot onto its 64-byte scratch
+  const uint32_t okmask = g < uint32_t(G) ? p.ring - 1 : 0u;
 
   const uint32_t lanes_real = p.W / R;          // host guarantees W % R == 0, lanes_real <= L
   const uint32_t VB = lanes_real * K;           // virtual bands down to the strip bottom
@@ -654,7 +818,7 @@ comb2_kernel(const CombParams p) {
           for (int k = 0; k < REM; ++k) tblr[(ab * 32 + lane) * REM + k] = wv[4 * Q4 + k];
         }
       }
-      for (uint32_t k = j; k < 2 * p.ring; k += L) okA[k] = 0;
+      for (uint32_t k = j; k <= okmask; k += L) sts_u32(okb + 4 * k, 0u);
     }
     __syncwarp();
 
@@ -758,7 +922,7 @@ comb2_kernel(const CombParams p) {
       ych = nxa;
       ych2 = nxb;
       __syncwarp();
-      extract_chunk<L, NB, DENSE>(p, ringB, okA, j, g, lane,
+      extract_chunk<L, NB, DENSE>(p, ringB, okb, okmask, j, g, lane,
                                   2 * (int32_t(ch * kChunk) - int32_t(VB - 1)), nseg_cols, kbase, c0, rA,
                                   rB, hasA, hasB, run, hitsA, hitsB);
       if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= kRebaseAt) {

@@ -29,10 +29,12 @@ __device__ __forceinline__ uint32_t smid() { uint32_t s; asm volatile("mov.u32 %
 #define HMAX(d, a, b) asm volatile("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
 #define HMIN(d, a, b) asm volatile("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
 #define HFMA(d, a, b, c) asm volatile("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c))
+#define HSETNE(d, a, b) asm volatile("set.ne.f16x2.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b))
+#define VADDMAX(d, a, b, c) asm volatile("{.reg .b32 t; add.s16x2 t, %1, %2; max.s16x2 %0, t, %3;}" : "=r"(d) : "r"(a), "r"(b), "r"(c))
 
 // Each VARIANT body updates v[i] with K ops (K returned by kops()).
 template <int V> __host__ __device__ constexpr int kops() {
-  return V == 0 ? 1 : V == 1 ? 2 : V == 2 ? 1 : V == 3 ? 1 : V == 4 ? 2 : V == 5 ? 1 : V == 6 ? 2 : V == 7 ? 2 : V == 8 ? 2 : V == 9 ? 3 : V == 10 ? 3 : V == 11 ? 3 : 2;
+  return V == 0 ? 1 : V == 1 ? 2 : V == 2 ? 1 : V == 3 ? 1 : V == 4 ? 2 : V == 5 ? 1 : V == 6 ? 2 : V == 7 ? 2 : V == 8 ? 2 : V == 9 ? 3 : V == 10 ? 3 : V == 11 ? 3 : V == 12 ? 2 : V == 13 ? 1 : V == 14 ? 2 : V == 15 ? 4 : V == 16 ? 3 : 2;
 }
 
 template <int V>
@@ -66,6 +68,18 @@ __global__ void k_ops(uint32_t* out, Rec* rec, uint32_t seed) {
       // comb cell (fp16 key, fp16 max): HMUL2, HMNMX2, LOP3
       if constexpr (V == 11) { uint32_t t = v[(i + CH - 1) % CH]; HMUL(d, t, b[i]); HMAX(e, v[i], d); LOP3(f, v[i], t, e); v[i] = f; }
       if constexpr (V == 12) { HFMA(d, v[i], b[i], c[i]); LOP3(e, d, b[i], c[i]); v[i] = e; }
+      if constexpr (V == 13) { HSETNE(d, v[i], b[i]); v[i] = d; }
+      // comb cell (viaddmax): d = max(T + A, V); V' = V ^ T ^ d                [alu, alu]
+      if constexpr (V == 14) { uint32_t t = v[(i + CH - 1) % CH]; d = __viaddmax_s16x2(t, b[i] & 0x80008000u, v[i]); LOP3(f, v[i], t, d); v[i] = f; }
+      // comb cell (computed mask): M = (x != y); t = T * M; d = max(V, t); V' = V ^ T ^ d  [fp16 set, hmul2, alu, alu]
+      if constexpr (V == 15) { uint32_t t = v[(i + CH - 1) % CH]; HSETNE(e, b[i], c[i]); HMUL(d, t, e); VMAX(e, v[i], d); LOP3(f, v[i], t, e); v[i] = f; }
+      // half of the cells each way (average 3 ops per cell)
+      if constexpr (V == 16) {
+        uint32_t t = v[(i + CH - 1) % CH];
+        if (i & 1) { HSETNE(e, b[i], c[i]); HMUL(d, t, e); VMAX(e, v[i], d); LOP3(f, v[i], t, e); }
+        else { d = __viaddmax_s16x2(t, b[i] & 0x80008000u, v[i]); LOP3(f, v[i], t, d); }
+        v[i] = f;
+      }
     }
   }
   __syncthreads();
@@ -92,6 +106,14 @@ __global__ void k_check(uint32_t* bad) {
       VMAX(vm, ka, kb); VMIN(vn, ka, kb);
       if (mx != vm) atomicAdd(bad + 2, 1);
       if (mn != vn) atomicAdd(bad + 3, 1);
+    }
+    if (a < 0x200u) {   // codes as fp16 bit patterns: set.ne is exact pattern inequality
+      for (uint32_t bb = 0; bb < 0x200u; ++bb) {
+        uint32_t r;
+        HSETNE(r, a | (bb << 16), bb | (bb << 16));
+        const uint32_t want = (a != bb ? 0x3C00u : 0u) | 0u;
+        if ((r & 0xFFFFu) != want || (r >> 16) != 0u) atomicAdd(bad + 4, 1);
+      }
     }
   }
 }
@@ -138,11 +160,15 @@ int main() {
     run(k_ops<9>, "cell(AND,VIMNMX,LOP3)", wps, kops<9>());
     run(k_ops<10>, "cell(HMUL2,VIMNMX,LOP3)", wps, kops<10>());
     run(k_ops<11>, "cell(HMUL2,HMNMX2,LOP3)", wps, kops<11>());
+    run(k_ops<13>, "HSET2", wps, kops<13>());
+    run(k_ops<14>, "cell(VIADDMAX,LOP3)", wps, kops<14>());
+    run(k_ops<15>, "cell(HSET2,HMUL2,VIMNMX,LOP3)", wps, kops<15>());
+    run(k_ops<16>, "cell(mixed 1:1)", wps, kops<16>());
   }
-  uint32_t* bad; cudaMalloc(&bad, 16); cudaMemset(bad, 0, 16);
+  uint32_t* bad; cudaMalloc(&bad, 32); cudaMemset(bad, 0, 32);
   k_check<<<256, 128>>>(bad);
-  uint32_t hb[4]; cudaMemcpy(hb, bad, 16, cudaMemcpyDeviceToHost);
-  printf("{\"fp16_check\": {\"mul_one_bad\": %u, \"mul_zero_bad\": %u, \"max_bad\": %u, \"min_bad\": %u}}\n", hb[0], hb[1], hb[2], hb[3]);
+  uint32_t hb[5]; cudaMemcpy(hb, bad, 20, cudaMemcpyDeviceToHost);
+  printf("{\"fp16_check\": {\"mul_one_bad\": %u, \"mul_zero_bad\": %u, \"max_bad\": %u, \"min_bad\": %u, \"set_ne_bad\": %u}}\n", hb[0], hb[1], hb[2], hb[3], hb[4]);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("{\"summary\": true, \"sms\": %d, \"clock_khz_attr\": %d, \"alu_lane_ops_per_clk_per_sm\": %.2f, \"name\": \"%s\"}\n",
          nsm, clk, best_alu, p.name);
