@@ -374,12 +374,17 @@ def run_engine(args, rank, world, local_rank):
             with open(NCU_TRAFFIC) as f:
                 traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
         cpc = cells_local / kern_max / (props.multi_processor_count * sm_mhz * 1e6)
-        ceiling = 64.0 / (0.75 if c.r == 2 else 1.0)
+        # generic kernel: VIADDMNMX + LOP3 per u32 (two strips x one cell) on the ALU pipe
+        #   -> peak_ops_clk cells/clk/SM;
+        # r = 2 kernel: per u32 block of two strips x (2 x 2 blown cells) 5 ALU ops (3 VIMNMX,
+        #   VIADDMNMX, LOP3; the $ x $ swap is free) + 2 IMAD -> 8 * peak_ops_clk / 5 cells/clk/SM
+        ceiling = peak_ops_clk * (8.0 / 5.0 if c.r == 2 else 1.0)
         roof = {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel_alu_bound": {"cells_per_clk_per_sm": cpc, "ceiling": ceiling, "frac": cpc / ceiling,
-                                     "what": "comb cells per SM clock vs this kernel's own ALU-pipe ceiling "
-                                             "(64 lane-ops/clk/SM at 2 ALU ops per cell pair; 0.75 per cell for r=2)"},
+                                     "what": "comb cells per SM clock vs this kernel's own instruction ceiling "
+                                             "(ALU pipe at the measured rate; r=1: 2 ALU ops per 2 cells (one u32 = two strips); "
+                                             "r=2: 5 ALU ops per 8 blown cells)"},
                 "basis": "3 int32 lane-ops per comb cell (SURVEY §8d), cells = rows*(w*r)*(n*r); peak = "
                          f"{props.multi_processor_count} SMs x {peak_ops_clk:.1f} measured lane-ops/clk/SM x "
                          f"{sm_mhz:.0f} MHz (median SM clock during the run)",
