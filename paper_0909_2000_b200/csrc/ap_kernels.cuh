@@ -155,6 +155,12 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void lds_v4(uint32_t addr, uint32_t* v) {
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void lds_v2(uint32_t addr, uint32_t* v) {
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr) : "memory");
+}
 __device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
 }
@@ -238,12 +244,14 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
 //    C = 0x8000 | (W - 1 + A); bit 15 of kk is then "not countable" and
 //    (kk + e - W + 1) mod ring is the flag slot -- for non-countable seaweeds
 //    the slot of start e + A, a start whose flag nobody has written yet.
-//  * Clear-ahead: each chunk zeroes the slots of starts [E0 + A, E0 + A + NB)
-//    (A = NB + (-E0 mod 32): 32-aligned, so whole lane runs are vector stores).
+//  * Clear-ahead: each chunk zeroes the slots of starts [E0 + A, E0 + A + NB).
 //    Those starts cannot have exited yet (A >= NB), so the stray flags of the
 //    chunk (all aimed inside this range) are wiped before the slot is used,
 //    and no per-seaweed select or branch is needed.  Live slots span
 //    W + NB + A <= W + 2 NB + 31 starts (ring_slots).
+//  * When L divides 32 and NB, slots are offset by delta so that every lane's
+//    run of CPL read slots and CPL cleared slots is CPL-aligned: one vector
+//    load / store per lane and no per-column wrap masks.
 //  * Slot addresses and the running count use IMAD / IMAD.HI on the FMA pipe.
 // Packed 32-bit sums are exact whenever every half of the final value is in
 // [0, 0xFFFF] (arithmetic is linear mod 2^32), so no per-column bias is needed.
@@ -254,18 +262,23 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
                                               uint32_t rA, uint32_t rB, bool hasA, bool hasB,
                                               uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
   constexpr int CPL = (NB + L - 1) / L;   // columns per lane (the last lane may get fewer real ones)
+  constexpr bool ALIGN = 32 % L == 0 && NB % L == 0;   // CPL is a power of two dividing 32
   const uint32_t rshift = p.r - 1;
   const uint32_t one = p.one;
+  const uint32_t k17 = one << 17, k18 = one << 18, k16 = one << 16;   // opaque: IMAD.HI, not LEA.HI
+  const int32_t W = int32_t(p.W);
   const int32_t eb = E0 + int32_t(j) * CPL;
-  const uint32_t A = NB + (uint32_t(-E0) & 31u);                    // E0 mod 32 is the same every chunk
+  // delta aligns the read runs (eb - W + delta) and clear runs (E0 + A + delta + j*CPL) to CPL
+  const uint32_t delta = ALIGN ? uint32_t(W - E0) & 31u : 0u;
+  const uint32_t A = NB + (ALIGN ? uint32_t(-W) & uint32_t(CPL - 1) : 0u);
   const uint32_t clamp2 = (0x8000u | (p.W - 1 + A)) * 0x00010001u;
   const uint32_t rmask2 = rmask * 0x00010001u;
-  const uint32_t n0 = (uint32_t(kbase + int32_t(p.W) - 1 - eb) & 0xFFFFu) * 0x00010001u;   // -(thr+1) at eb
-  const uint32_t sb2 = (uint32_t(eb - int32_t(p.W) + 1) & rmask) * 0x00010001u;            // slot of start eb-W+1
+  const uint32_t n0 = (uint32_t(kbase + W - 1 - eb) & 0xFFFFu) * 0x00010001u;          // -(thr+1) at eb
+  const uint32_t sb2 = (uint32_t(eb - W + 1 + int32_t(delta)) & rmask) * 0x00010001u;   // slot of start eb-W+1
   const uint32_t xA = okb * 0x00010001u + 0x20000u;   // addrA = imad(addrB, -65536, imad(slot2, 4, xA))
 
   // ---- phase 1: scatter the ok flags of countable seaweeds
-  uint32_t nc[CPL];   // bit 15 / 31: column not countable (strip A / B)
+  uint32_t cab[CPL];   // bit 15 / 31: column countable (strip A / B)
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
@@ -278,83 +291,148 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
     if (!valid) kk = clamp2;
     const uint32_t pre = kk + sb2 + uint32_t(c) * 0x00010001u;   // halves < 0x10000: no carry
     const uint32_t slot2 = pre & rmask2;
-    nc[c] = pre & 0x80008000u;
-    const uint32_t addrB = madhi(slot2, 1u << 18, okb + 2);     // okb + 4 * slotB + 2
+    cab[c] = ~pre & 0x80008000u;
+    const uint32_t addrB = madhi(slot2, k18, okb + 2);          // okb + 4 * slotB + 2
     const uint32_t addrA = imad(addrB, 0xFFFF0000u, imad(slot2, 4u, xA));   // okb + 4 * slotA
     sts_u8(addrA, 1u);
     sts_u8(addrB, 1u);
   }
   __syncwarp();
 
-  // ---- phase 2: read the flags of starts e - W; acc = sum(not countable + ok)
-  const uint32_t rsb = uint32_t(eb - int32_t(p.W)) & rmask;
-  uint32_t acc = 0;
+  // ---- phase 2: flags of starts e - W; acc = running sum of count deltas (countable - ok)
+  uint32_t o[CPL];
+  if constexpr (ALIGN) {
+    const uint32_t rb = okb + 4 * (uint32_t(eb - W + int32_t(delta)) & rmask);
+    if constexpr (CPL >= 4) {
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    const int32_t e = eb + c;
-    const bool real = NB % L == 0 || j * CPL + c < NB;
-    const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
-    uint32_t o = 0;
-    if ((!CHECK && NB % L == 0) || valid) o = lds_u32(okb + 4 * ((rsb + c) & rmask));
-    acc = imad(o, one, madhi(nc[c], 1u << 17, acc));   // acc + (nc >> 15) + o
-    nc[c] = acc;                                         // running sum after column c
-  }
-  // clear ahead: starts [E0 + A, E0 + A + NB), this lane's run of CPL
-  {
-    const uint32_t cb = uint32_t(E0 + int32_t(A) + int32_t(j) * CPL) & rmask;
-    if constexpr (NB % L == 0 && (CPL == 4 || CPL == 8 || CPL == 16)) {
-#pragma unroll
-      for (int q = 0; q < CPL / 4; ++q) sts_zero_v4(okb + 4 * cb + 16 * q);
-    } else if constexpr (NB % L == 0 && CPL == 2) {
-      sts_zero_v2(okb + 4 * cb);
+      for (int q = 0; q < CPL / 4; ++q) lds_v4(rb + 16 * q, o + 4 * q);
+    } else if constexpr (CPL == 2) {
+      lds_v2(rb, o);
     } else {
+      o[0] = lds_u32(rb);
+    }
+    if constexpr (CHECK) {
 #pragma unroll
       for (int c = 0; c < CPL; ++c)
-        if (NB % L == 0 || j * CPL + c < NB) sts_u32(okb + 4 * ((cb + c) & rmask), 0u);
+        if (!(eb + c >= 0 && eb + c < int32_t(nseg_cols))) o[c] = 0u;
     }
-  }
-  // lane total of count deltas (1 - nc - o per real column; invalid columns add 0)
-  const uint32_t tot = uint32_t(CPL) * 0x00010001u - acc;
-  uint32_t incl = tot;
-#pragma unroll
-  for (int off = 1; off < L; off <<= 1) {
-    const uint32_t v = shfl_up_n<L>(incl, off);
-    if (j >= uint32_t(off)) incl += v;
-  }
-  // count after column c = runc + c * 0x10001 - sum_c;  half = Kh - 2 * count
-  const uint32_t runc = run + incl - tot + 0x00010001u;
-  run = shfl_group_last<L>(run + incl, g);
-  const uint32_t kh = (2 * p.W - (rshift ? 2 * p.w : 0u)) * 0x00010001u;
-  if constexpr (DENSE) {
-    // packed halves biased by 0x8000 (r = 2 scores can be negative)
-    const uint32_t kb = imad(runc, 0xFFFFFFFEu, kh + 0x80008000u);
+  } else {
+    const uint32_t rsb = uint32_t(eb - W) & rmask;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const int32_t e = eb + c;
       const bool real = NB % L == 0 || j * CPL + c < NB;
       const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
-      const int32_t kp = e - int32_t(p.W) + 1;   // window start (segment-relative)
-      const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
-      const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
-      const uint32_t hb = imad(nc[c], 2u, kb - uint32_t(2 * c) * 0x00010001u);   // (h + 0x8000) per half
-      const uint32_t hlo = hb - 0x8000u;                       // low 16 bits: hA
-      const uint32_t hhi = madhi(hb, 0x10000u, 0xFFFF8000u);   // low 16 bits: hB
-      if (p.out_kind == 0) {
-        if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hlo);
-        if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hhi);
-      } else if (p.out_kind == 2) {   // compact: half-units as bytes (w <= 127)
-        if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(hlo);
-        if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(hhi);
+      o[c] = 0u;
+      if (valid) o[c] = lds_u32(okb + 4 * ((rsb + c) & rmask));
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    acc = imad(o[c], 0xFFFFFFFFu, madhi(cab[c], k17, acc));   // acc + countable - ok
+    cab[c] = acc;                                            // count delta through column c
+  }
+  // clear ahead: starts [E0 + A, E0 + A + NB), this lane's run of CPL
+  {
+    if constexpr (ALIGN) {
+      const uint32_t cb = okb + 4 * (uint32_t(E0 + int32_t(A + delta) + int32_t(j) * CPL) & rmask);
+      if constexpr (CPL >= 4) {
+#pragma unroll
+        for (int q = 0; q < CPL / 4; ++q) sts_zero_v4(cb + 16 * q);
+      } else if constexpr (CPL == 2) {
+        sts_zero_v2(cb);
       } else {
-        // write_pgm (io.cpp:136-153): pixel = (255*clamp(h,0,2w) + w) / 2w, cut -> 0
-        const int32_t hA = int32_t(int16_t(uint16_t(hlo))), hB = int32_t(int16_t(uint16_t(hhi)));
-        const int32_t full = 2 * int32_t(p.w);
-        const bool cutA = p.has_pgm_threshold && hA < p.pgm_threshold;
-        const bool cutB = p.has_pgm_threshold && hB < p.pgm_threshold;
-        const int32_t qA = cutA ? 0 : (255 * min(max(hA, 0), full) + full / 2) / full;
-        const int32_t qB = cutB ? 0 : (255 * min(max(hB, 0), full) + full / 2) / full;
-        if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(qA);
-        if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(qB);
+        sts_u32(cb, 0u);
+      }
+    } else {
+      const uint32_t cb = uint32_t(E0 + int32_t(A) + int32_t(j) * CPL) & rmask;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        if (NB % L == 0 || j * CPL + c < NB) sts_u32(okb + 4 * ((cb + c) & rmask), 0u);
+    }
+  }
+  // group scan of the lane totals; count after column c = run + excl + acc_c
+  uint32_t incl = acc;
+#pragma unroll
+  for (int off = 1; off < L; off <<= 1) {
+    const uint32_t v = shfl_up_n<L>(incl, off);
+    if (j >= uint32_t(off)) incl += v;
+  }
+  const uint32_t runc = run + incl - acc;
+  run = shfl_group_last<L>(run + incl, g);
+  const uint32_t kh = (2 * p.W - (rshift ? 2 * p.w : 0u)) * 0x00010001u;   // half = kh - 2 * count
+  const int32_t kp0 = eb - W + 1;   // window start of column eb (segment-relative)
+  if constexpr (DENSE) {
+    // packed halves biased by 0x8000 (r = 2 scores can be negative)
+    const uint32_t kb = imad(runc, 0xFFFFFFFEu, kh + 0x80008000u);
+    if (!CHECK && p.out_kind != 1) {
+      // interior chunk: every column valid; r = 2 reports the columns with c = par (mod 2)
+      const uint32_t par = uint32_t(kp0) & rshift;
+      const size_t gb = (c0 + uint32_t(kp0) + par) >> rshift;   // output column of the first reported c
+      if (p.out_kind == 0) {
+        uint16_t* pa = p.out + size_t(rA) * p.cols + gb;
+        uint16_t* pb = p.out + size_t(rB) * p.cols + gb;
+        if (rshift == 0) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            if (NB % L != 0 && j * CPL + c >= NB) continue;
+            const uint32_t hb = imad(cab[c], 0xFFFFFFFEu, kb);
+            if (hasA) pa[c] = uint16_t(hb - 0x8000u);
+            if (hasB) pb[c] = uint16_t(madhi(hb, k16, 0xFFFF8000u));
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            if (NB % L != 0 && j * CPL + c >= NB) continue;
+            if ((uint32_t(c) & 1u) != par) continue;
+            const uint32_t hb = imad(cab[c], 0xFFFFFFFEu, kb);
+            if (hasA) pa[c >> 1] = uint16_t(hb - 0x8000u);
+            if (hasB) pb[c >> 1] = uint16_t(madhi(hb, k16, 0xFFFF8000u));
+          }
+        }
+      } else {   // compact: half-units as bytes (w <= 127)
+        uint8_t* pa = p.out8 + size_t(rA) * p.cols + gb;
+        uint8_t* pb = p.out8 + size_t(rB) * p.cols + gb;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          if (NB % L != 0 && j * CPL + c >= NB) continue;
+          if ((uint32_t(c) & rshift) != par) continue;
+          const uint32_t hb = imad(cab[c], 0xFFFFFFFEu, kb);
+          const uint32_t off = uint32_t(c) >> rshift;
+          if (hasA) pa[off] = uint8_t(hb - 0x8000u);
+          if (hasB) pb[off] = uint8_t(madhi(hb, k16, 0xFFFF8000u));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int32_t e = eb + c;
+        const bool real = NB % L == 0 || j * CPL + c < NB;
+        const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
+        const int32_t kp = kp0 + c;
+        const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
+        const uint32_t gcol = (c0 + uint32_t(kp)) >> rshift;
+        const uint32_t hb = imad(cab[c], 0xFFFFFFFEu, kb);   // (h + 0x8000) per half
+        const uint32_t hlo = hb - 0x8000u;                       // low 16 bits: hA
+        const uint32_t hhi = madhi(hb, k16, 0xFFFF8000u);        // low 16 bits: hB
+        if (p.out_kind == 0) {
+          if (out_ok && hasA) p.out[size_t(rA) * p.cols + gcol] = uint16_t(hlo);
+          if (out_ok && hasB) p.out[size_t(rB) * p.cols + gcol] = uint16_t(hhi);
+        } else if (p.out_kind == 2) {
+          if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(hlo);
+          if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(hhi);
+        } else {
+          // write_pgm (io.cpp:136-153): pixel = (255*clamp(h,0,2w) + w) / 2w, cut -> 0
+          const int32_t hA = int32_t(int16_t(uint16_t(hlo))), hB = int32_t(int16_t(uint16_t(hhi)));
+          const int32_t full = 2 * int32_t(p.w);
+          const bool cutA = p.has_pgm_threshold && hA < p.pgm_threshold;
+          const bool cutB = p.has_pgm_threshold && hB < p.pgm_threshold;
+          const int32_t qA = cutA ? 0 : (255 * min(max(hA, 0), full) + full / 2) / full;
+          const int32_t qB = cutB ? 0 : (255 * min(max(hB, 0), full) + full / 2) / full;
+          if (out_ok && hasA) p.out8[size_t(rA) * p.cols + gcol] = uint8_t(qA);
+          if (out_ok && hasB) p.out8[size_t(rB) * p.cols + gcol] = uint8_t(qB);
+        }
       }
     }
   } else {
@@ -362,7 +440,7 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
     const uint32_t kt = imad(runc, 0xFFFFFFFEu, kh + (0x8000u - uint32_t(p.t_half)) * 0x00010001u);
     uint32_t any = 0;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) any |= imad(nc[c], 2u, kt - uint32_t(2 * c) * 0x00010001u);
+    for (int c = 0; c < CPL; ++c) any |= imad(cab[c], 0xFFFFFFFEu, kt);
     // Row-major ranks: a hit's rank in its (row, segment) = the row's earlier
     // hits (previous chunks, lower lanes of this chunk, lower columns of this lane).
     if (__any_sync(0xFFFFFFFFu, any & 0x80008000u)) {
@@ -372,9 +450,9 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
         const int32_t e = eb + c;
         const bool real = NB % L == 0 || j * CPL + c < NB;
         const bool valid = real && (!CHECK || (e >= 0 && e < int32_t(nseg_cols)));
-        const int32_t kp = e - int32_t(p.W) + 1;
+        const int32_t kp = kp0 + c;
         const bool out_ok = valid && (!CHECK || (kp >= 0 && kp < int32_t(p.S))) && !(uint32_t(kp) & rshift);
-        const uint32_t ht = imad(nc[c], 2u, kt - uint32_t(2 * c) * 0x00010001u);
+        const uint32_t ht = imad(cab[c], 0xFFFFFFFEu, kt);
         hmA |= uint32_t(out_ok && hasA && (ht & 0x8000u)) << c;
         hmB |= uint32_t(out_ok && hasB && (ht & 0x80000000u)) << c;
       }
@@ -402,8 +480,8 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
       const uint32_t kb = imad(runc, 0xFFFFFFFEu, kh + 0x80008000u);
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        const uint32_t gcol = (c0 + uint32_t(eb + c - int32_t(p.W) + 1)) >> rshift;
-        const uint32_t hb = imad(nc[c], 2u, kb - uint32_t(2 * c) * 0x00010001u);
+        const uint32_t gcol = (c0 + uint32_t(kp0 + c)) >> rshift;
+        const uint32_t hb = imad(cab[c], 0xFFFFFFFEu, kb);
         const uint32_t hA = uint32_t(int32_t(hb & 0xFFFFu) - 0x8000), hB = uint32_t(int32_t(hb >> 16) - 0x8000);
         if ((hmA >> c) & 1u) {
           if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hA & 0xFFFFu, rkA);
