@@ -251,3 +251,50 @@ def test_multi_device_row_shards(ndev, monkeypatch):
         # a row range split across shards
         part = ap.plot_dense_u16(x, y, cfg(w, h, r, n_devices=ndev), 7, 7 + 2 * ndev + 5)
         assert np.array_equal(part, one[7:7 + 2 * ndev + 5])
+
+
+@pytest.mark.parametrize("w,r,h,sigma", [(64, 1, 1, 4), (128, 1, 2, 4), (256, 1, 1, 4), (33, 1, 1, 4), (255, 1, 3, 2),
+                                         (100, 2, 1, 4), (64, 2, 1, 20), (512, 2, 1, 4), (7, 2, 2, 4)])
+def test_long_sequences_dense_and_threshold(w, r, h, sigma):
+    """Long y (many interior extraction chunks, several key rebases per strip) with
+    planted homology: dense grid and thresholded lists bit-exact, including
+    thresholds outside the score range (the kernel clamps t to +-0x4000)."""
+    rng = np.random.default_rng(w * 7 + r * 3 + sigma)
+    m = w + 5 * h
+    x = rng.integers(1, sigma + 1, m).astype(np.uint8)
+    parts = []
+    while sum(p.size for p in parts) < 70000:
+        parts.append(rng.integers(1, sigma + 1, int(rng.integers(50, 3000))).astype(np.uint8))
+        blk = x[int(rng.integers(0, max(1, m - w))):][:w + 20].copy()
+        flip = rng.random(blk.size) < 0.08
+        blk[flip] = rng.integers(1, sigma + 1, int(flip.sum()))
+        parts.append(blk)
+    y = np.concatenate(parts)
+    rc, want = ol.plot_rows(x, y, w, h, r)
+    assert rc == 0
+    got = gpu_grid(x, y, w, h, r)
+    assert np.array_equal(got, want)
+    for t in (int(np.quantile(want, 0.999)), int(want.max()), int(want.min()) - 3, 5000, -5000):
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc), (t, gr.size, rr.size)
+        assert np.array_equal(gh, want[rr, cc]), t
+
+
+@pytest.mark.parametrize("shape", ["8,16,4", "16,8,2", "32,8,2"])
+def test_forced_generic_shapes_long_y(shape, monkeypatch):
+    """Forced generic shapes on a y long enough for interior chunks and rebases, both r."""
+    monkeypatch.setenv("AP_SHAPE", shape)
+    monkeypatch.setenv("AP_NO_R2", "1")
+    L, R, K = map(int, shape.split(","))
+    rng = np.random.default_rng(L * 100 + R)
+    for r in (1, 2):
+        w = max(2, min((L * R) // r - 1, 200))
+        x = rng.integers(1, 5, w + 9).astype(np.uint8)
+        y = np.concatenate([rng.integers(1, 5, 30000), x[:w], rng.integers(1, 5, 3000)]).astype(np.uint8)
+        rc, want = ol.plot_rows(x, y, w, 1, r)
+        assert np.array_equal(gpu_grid(x, y, w, 1, r), want), (shape, r)
+        t = int(np.quantile(want, 0.999))
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
