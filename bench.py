@@ -166,7 +166,8 @@ def reference_rows_rate(c, x, y, budget_s: float, max_rows: int):
 
 
 def run_reference(args, rank, world):
-    c, x, y = workload(args.config, 1)
+    # the same workload as the engine arm at this world size (weak scaling grows x), sampled by rows
+    c, x, y = workload(args.config, world)
     rows_total, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
     metric_unit = "window-pair cell updates/s"
     if rank != 0:
@@ -191,7 +192,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * t_all / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (paper_0909_2000_b200.datagen)",
-        "config": config_desc(c, x, y, 1, args.config),
+        "config": dict(config_desc(c, x, y, world, args.config),
+                       parallelism=f"reference CPU on rank 0 ({cores} host threads)"),
         "cpu_baseline": {"value": value, "unit": metric_unit, "cores": cores, "kind": "reference",
                          "sample": desc},
         "e2e": {"value": value, "unit": metric_unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
