@@ -417,6 +417,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   if (ngroups < want) nseg = (want + ngroups - 1) / ngroups;
   const size_t min_seg = std::max<size_t>(4 * W, 256);
   nseg = std::min(nseg, std::max<size_t>(1, out_cols_eff / min_seg));
+  if (const char* e = std::getenv("AP_NSEG")) nseg = std::max<size_t>(1, std::strtoull(e, nullptr, 10));   // tuning
   size_t S = (out_cols_eff + nseg - 1) / nseg;
   // segment starts aligned for 16-B vector loads of the code stream (raw codes
   // for the r = 2 kernel: blown starts multiple of 64)
