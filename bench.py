@@ -76,8 +76,13 @@ class ClockSampler:
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # wait until the sampler is live so short timed regions are covered too
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.start = len(self.lines)
         return self
 
     def _read(self):
@@ -85,6 +90,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.proc:
+            # a region shorter than the 50 ms period: take the first sample after it
+            # (still at the load clocks, before the GPU idles down)
+            t0 = time.perf_counter()
+            while len(self.lines) <= self.start and time.perf_counter() - t0 < 0.2:
+                time.sleep(0.002)
+        self.lines = self.lines[self.start:]
         if self.proc:
             self.proc.terminate()
             try:
