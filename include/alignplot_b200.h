@@ -82,6 +82,20 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
                       uint64_t* count, uint32_t* rows, uint32_t* cols, uint16_t* halves,
                       size_t cap);
 
+/* One thresholded cell (PlotCell, scoring.hpp:33-42) for the array-of-structs
+ * form below. */
+typedef struct ap_cell {
+  uint32_t row;   /* grid row (global) */
+  uint32_t col;   /* grid column */
+  int32_t half;   /* half-unit score */
+} ap_cell;
+
+/* As ap_plot_threshold, filling ap_cell records -- the PlotCell list
+ * apply_threshold returns (scoring.cpp:30-39) -- instead of parallel arrays;
+ * same count / cap / AP_CAPACITY contract. */
+int ap_plot_threshold_cells(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                            uint64_t* count, ap_cell* cells, size_t cap);
+
 /* As ap_plot_dense with the half-unit scores stored as bytes (lossless for
  * w <= 127, where scores lie in [0, 2w]; AP_CONFIG otherwise): half the
  * device-to-host bytes of the uint16 layout. */

@@ -22,11 +22,17 @@ AP_MAX_BLOWN_WINDOW = 1024
 # Every symbol declared in include/alignplot_b200.h (checked by tests/test_abi.py).
 EXPORTS = (
     "ap_grid_dims", "ap_validate", "ap_plot_dense", "ap_plot_dense_u8", "ap_plot_threshold", "ap_plot_pgm",
+    "ap_plot_threshold_cells",
     "ap_last_error",
     "ap_device_count", "ap_ctx_create", "ap_ctx_destroy", "ap_ctx_plot_dense_device",
     "ap_ctx_plot_threshold_device", "ap_ctx_plot_pgm_device", "ap_ctx_plot_dense_u8_device",
     "ap_ctx_last_kernel_ms", "ap_ctx_last_launches",
 )
+
+
+class ApCell(ctypes.Structure):
+    """ap_cell (include/alignplot_b200.h): one thresholded cell, PlotCell (scoring.hpp:33-42)."""
+    _fields_ = [("row", c_uint32), ("col", c_uint32), ("half", c_int32)]
 
 
 class ApConfig(ctypes.Structure):
@@ -65,6 +71,9 @@ def lib() -> ctypes.CDLL:
     L.ap_plot_threshold.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig),
                                     POINTER(c_uint64), c_void_p, c_void_p, c_void_p, c_size_t]
     L.ap_plot_threshold.restype = c_int
+    L.ap_plot_threshold_cells.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig),
+                                          POINTER(c_uint64), c_void_p, c_size_t]
+    L.ap_plot_threshold_cells.restype = c_int
     L.ap_plot_dense_u8.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig), c_void_p]
     L.ap_plot_dense_u8.restype = c_int
     L.ap_ctx_plot_dense_u8_device.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t,

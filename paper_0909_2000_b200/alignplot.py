@@ -333,6 +333,26 @@ def plot_threshold_arrays(x, y, cfg: PlotConfig, t_half: int, cap: Optional[int]
         return r[:n], k[:n], hv[:n]
 
 
+def plot_threshold_cells(x, y, cfg: PlotConfig, t_half: int, row_begin: int = 0, row_end: int = 0) -> List[PlotCell]:
+    """The same list through the array-of-structs entry point ap_plot_threshold_cells."""
+    xa, ya = _codes(x), _codes(y)
+    c = _cfg(cfg, row_begin, row_end)
+    c.has_threshold = 1
+    c.threshold_half = int(t_half)
+    L = _native.lib()
+    count = ctypes.c_uint64(0)
+    cap = 1 << 12
+    while True:
+        buf = (_native.ApCell * max(cap, 1))()
+        rc = L.ap_plot_threshold_cells(_ptr(xa), xa.size, _ptr(ya), ya.size, ctypes.byref(c), ctypes.byref(count),
+                                       ctypes.cast(buf, ctypes.c_void_p), cap)
+        if rc == _native.AP_CAPACITY:
+            cap = int(count.value)
+            continue
+        _raise(rc)
+        return [PlotCell(int(buf[i].row), int(buf[i].col), int(buf[i].half)) for i in range(int(count.value))]
+
+
 def compute_plot_threshold(x: Sequence, y: Sequence, cfg: PlotConfig, t_half: Optional[int] = None) -> List[PlotCell]:
     """apply_threshold(compute_plot(x, y, cfg), t) fused on the GPU (no dense grid is materialised)."""
     t = cfg.threshold_half if t_half is None else t_half

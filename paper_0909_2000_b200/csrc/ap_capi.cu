@@ -919,4 +919,18 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
   return host_plot(x, m, y, n, cfg, false, nullptr, count, rows, cols, halves, cap);
 }
 
+int ap_plot_threshold_cells(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                            uint64_t* count, ap_cell* cells, size_t cap) {
+  if (!count) return fail(AP_INVALID, "null count");
+  if (cap && !cells) return fail(AP_INVALID, "null output array");
+  if (!cfg || !cfg->has_threshold) return fail(AP_INVALID, "ap_plot_threshold_cells needs has_threshold");
+  std::vector<uint32_t> rows(cap), cols(cap);
+  std::vector<uint16_t> halves(cap);
+  const int rc = host_plot(x, m, y, n, cfg, false, nullptr, count, rows.data(), cols.data(), halves.data(), cap);
+  if (rc != AP_OK && rc != AP_CAPACITY) return rc;
+  const size_t k = std::min<uint64_t>(*count, cap);
+  for (size_t i = 0; i < k; ++i) cells[i] = ap_cell{rows[i], cols[i], int32_t(int16_t(halves[i]))};
+  return rc;
+}
+
 }  // extern "C"

@@ -298,3 +298,19 @@ def test_forced_generic_shapes_long_y(shape, monkeypatch):
         rr, cc = np.nonzero(want >= t)
         gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
         assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
+
+
+def test_threshold_cells_aos_matches_soa():
+    """ap_plot_threshold_cells (array of ap_cell) == ap_plot_threshold (parallel arrays),
+    including the AP_CAPACITY retry and both score modes."""
+    rng = np.random.default_rng(91)
+    x = rng.integers(1, 5, 1500).astype(np.uint8)
+    y = np.concatenate([rng.integers(1, 5, 300), x[200:900], rng.integers(1, 5, 200)]).astype(np.uint8)
+    for w, h, r in ((40, 1, 1), (25, 2, 2)):
+        rc, grid = ol.plot_rows(x, y, w, h, r)
+        t = int(np.quantile(grid, 0.99))
+        cells = ap.plot_threshold_cells(x, y, cfg(w, h, r), t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
+        assert len(cells) == gr.size > 100
+        assert [c.row for c in cells] == gr.tolist() and [c.col for c in cells] == gc.tolist()
+        assert [c.half for c in cells] == grid[gr, gc].tolist()
