@@ -313,4 +313,4 @@ def test_threshold_cells_aos_matches_soa():
         gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
         assert len(cells) == gr.size > 100
         assert [c.row for c in cells] == gr.tolist() and [c.col for c in cells] == gc.tolist()
-        assert [c.half for c in cells] == grid[gr, gc].tolist()
+        assert [c.score_half for c in cells] == grid[gr, gc].tolist()
