@@ -136,12 +136,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
-#ifndef AP_KH
-#define AP_KH 0
-#endif
-#ifndef AP_YUNI
-#define AP_YUNI 0
-#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -175,21 +169,6 @@ __device__ __forceinline__ void sts_zero_v4(uint32_t addr) {
 __device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-
-// fp16x2 inequality as 1.0 / 0.0 per half (HSET2.BF); codes compared as fp16 bit
-// patterns (0..0x1FF, never NaN, no FTZ for f16: tools/int_peak.cu set_ne check)
-__device__ __forceinline__ uint32_t hset2_ne(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("set.ne.f16x2.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
-
-// fp16x2 product (keys are positive finite fp16 patterns: k * 1.0 = k, k * 0 = +0)
-__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
 
@@ -550,9 +529,6 @@ comb_kernel(const CombParams p) {
   constexpr int RB = R / K;       // rows per band
   constexpr int QB = RB / 4;      // quads per band
   constexpr int VB = L * K;       // virtual bands per strip (wavefront depth)
-  // the last KH bands compute their masks on the fp16 pipe (HSET2 + HMUL2) instead
-  // of reading the table: fewer shared-memory wavefronts per cell
-  constexpr int KH = XM ? 0 : (AP_KH < K ? AP_KH : K - 1);
   constexpr uint32_t kTblMul = uint32_t(Q * L * 16) << 16;   // (code * 0x10001) -> code * table stride
   extern __shared__ __align__(16) unsigned char smem[];
 
@@ -587,7 +563,6 @@ comb_kernel(const CombParams p) {
     // ---- mismatch table / x-code registers (fused $-interleave, scoring.cpp:5-17)
     __syncwarp();
     uint32_t xpair[XM ? R : 1];
-    uint32_t xh[KH > 0 ? KH * RB : 1];   // x code pairs of the computed-mask bands (fp16 patterns)
     {
       uint32_t xa[R], xb[R];
 #pragma unroll
@@ -613,8 +588,6 @@ comb_kernel(const CombParams p) {
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) xpair[rho] = xa[rho] | (xb[rho] << 16);
       } else {
-#pragma unroll
-        for (int i = 0; i < KH * RB; ++i) xh[i] = xa[(K - KH) * RB + i] | (xb[(K - KH) * RB + i] << 16);
         uint4* tg = tbl + size_t(g) * p.sigma * Q * L;
         for (uint32_t a = 0; a < p.sigma; ++a) {
 #pragma unroll
@@ -635,12 +608,7 @@ comb_kernel(const CombParams p) {
 
     // table base of this lane; y column words are byte offsets of a code's quads
     const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + size_t(g) * p.sigma * Q * L + j));
-#if AP_YUNI
-    const uint4* yq = reinterpret_cast<const uint4*>(p.ycol + c0);   // warp-uniform loads
-    const uint32_t zj = j == 0 ? 1u : 0u;
-#else
     const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
-#endif
     // lane-select constants: the band-0 inputs are imad(shuffled, nz, own) on the
     // FMA pipe instead of selects (own = fresh key / new column word on lane 0, 0 elsewhere)
     const uint32_t nz = j != 0 ? 1u : 0u;
@@ -663,11 +631,7 @@ comb_kernel(const CombParams p) {
     // group lane 0's y words: a queue of the next 16 columns, refilled 8 at a time
     // (register moves and IMADs only: no byte extraction on the ALU pipe)
     uint4 qa = __ldg(yq), qb = __ldg(yq + 1), qc = __ldg(yq + 2), qd = __ldg(yq + 3);
-#if AP_YUNI
-    cd[0] = qa.x * zj;
-#else
     cd[0] = qa.x;                                      // column 0 (0 on lanes j != 0)
-#endif
     uint32_t nsub = 0;
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
@@ -681,7 +645,7 @@ comb_kernel(const CombParams p) {
           uint4 nfq[Q];
           if constexpr (!XM) {
 #pragma unroll
-            for (int b = 0; b < K - KH; ++b)
+            for (int b = 0; b < K; ++b)
 #pragma unroll
               for (int qq = 0; qq < QB; ++qq)
                 nfq[b * QB + qq] = lds128(madhi(cd[b], tblmul, tlb) + (b * QB + qq) * L * 16);
@@ -699,18 +663,6 @@ comb_kernel(const CombParams p) {
           for (int b = 0; b < K; ++b) {
             uint32_t t = tin[b];
             const uint32_t yrep = cd[b];                 // code * 0x10001
-            if (!XM && b >= K - KH) {
-#pragma unroll
-              for (int k = 0; k < RB; ++k) {
-                uint32_t& v = V[b * RB + k];
-                const uint32_t mm = hset2_ne(xh[(b - (K - KH)) * RB + k], yrep);   // 1.0 where codes differ
-                const uint32_t d = __vmaxu2(hmul2(t, mm), v);                      // match: max(0, V) = V
-                v = lop3_xor(v, t, d);
-                t = d;
-              }
-              tb[b] = t;
-              continue;
-            }
 #pragma unroll
             for (int qq = 0; qq < QB; ++qq) {
               uint32_t m[4];
@@ -740,11 +692,7 @@ comb_kernel(const CombParams p) {
             const uint32_t sh = shfl_up1<L>(cd[K - 1]);
 #pragma unroll
             for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
-#if AP_YUNI
-            cd[0] = imad(sh, nz, imad(ynew, zj, 0u));
-#else
             cd[0] = imad(sh, nz, ynew);
-#endif
           }
         }
         qa = qc; qb = qd; qc = na; qd = nb;
