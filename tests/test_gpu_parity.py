@@ -314,3 +314,35 @@ def test_threshold_cells_aos_matches_soa():
         assert len(cells) == gr.size > 100
         assert [c.row for c in cells] == gr.tolist() and [c.col for c in cells] == gc.tolist()
         assert [c.score_half for c in cells] == grid[gr, gc].tolist()
+
+
+def test_host_api_concurrent_threads():
+    """The host API is reentrant: concurrent calls from several threads (one shared
+    per-device context, serialised inside the library) give the serial results."""
+    import threading
+    rng = np.random.default_rng(123)
+    cases = []
+    for k in range(6):
+        w = int(rng.integers(8, 90))
+        x = rng.integers(1, 5, w + 200).astype(np.uint8)
+        y = rng.integers(1, 5, w + 900).astype(np.uint8)
+        cases.append((x, y, w, 1 + k % 3, 1 + k % 2))
+    want = [gpu_grid(*c) for c in cases]
+    got = [None] * len(cases)
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                got[i] = gpu_grid(*cases[i])
+        except Exception as e:   # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(cases))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
