@@ -136,6 +136,9 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+#ifndef AP_FMAMIN_RR
+#define AP_FMAMIN_RR 4   // r = 2 kernels with RR >= this compute one mismatch min with IMADs (C4: -1.3%)
+#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -771,7 +774,7 @@ comb2_kernel(const CombParams p) {
   constexpr int BW = r2_band_words(RRB);
   constexpr int Q4 = RRB / 4, REM = RRB % 4;
   constexpr int NB = 2 * kChunk;   // blown bottom columns per chunk
-  constexpr bool kFmaMin = RR >= 8;  // one of the two mismatch mins moves to the FMA pipe
+  constexpr bool kFmaMin = RR >= AP_FMAMIN_RR;  // one of the two mismatch mins moves to the FMA pipe
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
