@@ -188,13 +188,6 @@ __device__ __forceinline__ uint32_t lop3_xor(uint32_t a, uint32_t b, uint32_t c)
   return d;
 }
 
-// PRMT with sign replication (selector nibble bit 3); __byte_perm masks it off.
-__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t sel) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(a), "r"(sel));
-  return d;
-}
-
 // Shared memory bytes per warp: mismatch table (table_words 32-bit words per
 // lane per code), the bottom-key ring (nb entries per chunk, padded by one word
 // per group so the bottom lanes of different groups hit different banks) and
@@ -509,19 +502,19 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 // at step s, so the K chains of a lane are independent within a step (ILP K);
 // band 0 gets the seaweed leaving lane j-1's last band one step earlier via
 // SHFL, band b>0 the one its own band b-1 produced one step earlier.  The y
-// codes travel the same way, one step ahead, so the mismatch-table rows of
-// step s+1 are loaded from shared memory during step s.
+// codes travel the same way, one step ahead, so a step's table rows can be
+// loaded as soon as the step starts.
 //
-// XM = false (small alphabets): per-warp table M[code][row] holding, per
-//   16-bit half, the fp16 multiplier 1.0 (0x3C00, mismatch) or 0 (match);
-//   t = T * M runs as HFMA2 on the FMA pipe, so a cell pair costs
-//   HFMA2 + VIMNMX.U16x2 + LOP3 (two ALU-pipe ops).  Keys stay in [0, 0x7BFF]
-//   (positive finite fp16 patterns: x*1 = x, x*0 = +0, verified on B200 by
-//   tools/int_peak.cu).
-// XM = true (any alphabet): NF computed from the x-code pair registers:
-//   e = (xpair ^ y*0x10001) + 0x7FFF7FFF has bit 15 of a half set iff the
-//   codes differ; PRMT's sign-replicate mode (selector 0xBB99) widens it to
-//   0xFFFF; t = T & NF.
+// Cell (both strips in 16-bit halves): d = max_s16(T + A, V) (VIADDMNMX),
+// V' = V ^ T ^ d (LOP3), with A = 0x8000 (-32768) on a match and 0 otherwise:
+// two ALU-pipe ops per cell pair.  Keys stay in [0, 0x7BFF], so T - 32768 < 0
+// <= V on a match.
+// XM = false (small alphabets): per-group table M[code][row] of the A words,
+//   laid out [group][code][quad][lane] (conflict-free LDS.128); the y column
+//   word code * 0x10001 gives the table offset by one IMAD.HI.
+// XM = true (any alphabet): A computed from the x-code pair registers:
+//   A = ~((xpair ^ y * 0x10001) + 0x7FFF7FFF) & 0x80008000 (bit 15 of a half
+//   survives iff the codes are equal).
 template <int L, int R, int K, bool DENSE, bool XM>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
