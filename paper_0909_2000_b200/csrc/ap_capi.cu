@@ -90,12 +90,12 @@ struct Shape {
 // masks] + ~14 per-step overhead) + ~25 extraction ops, scaled up when fewer than
 // 16 warps per SM fit (registers from the compiled kernel, table in shared memory).
 bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
-  const uint32_t ring = apk::ring_slots(W, apk::kChunk);
   // tuning override: AP_SHAPE="L,R,K[,xm]"
   if (const char* env = std::getenv("AP_SHAPE")) {
     int l = 0, r = 0, k = 0, xm = 0;
     if (std::sscanf(env, "%d,%d,%d,%d", &l, &r, &k, &xm) >= 3 && pick_kernel(l, r, k, dense, xm) &&
         uint32_t(l * r) >= W) {
+      const uint32_t ring = apk::ring_slots(W, apk::kChunk, l);
       out->L = l; out->R = r; out->K = k; out->xm = xm; out->ring = ring;
       out->smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(l, r, xm ? 0 : sigma, ring);
       out->warps_per_sm = 0;
@@ -113,6 +113,7 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
         cudaGetLastError();
         continue;
       }
+      const uint32_t ring = apk::ring_slots(W, apk::kChunk, d.L);
       const size_t smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(d.L, d.R, xm ? 0 : sigma, ring);
       if (smem > kSmemPerSm - 1024) continue;
       const int by_regs = 65536 / (std::max(fa.numRegs, 1) * 32 * apk::kWarpsPerCta);
@@ -151,12 +152,12 @@ constexpr Shape2Def kShapes2[] = {
 bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
   if (std::getenv("AP_NO_R2")) return false;
   const uint32_t W = 2 * w;
-  const uint32_t ring = apk::ring_slots(W, 2 * apk::kChunk);
   // tuning override: AP_SHAPE2="L,RR,K"
   if (const char* env = std::getenv("AP_SHAPE2")) {
     int l = 0, rr = 0, k = 0;
     if (std::sscanf(env, "%d,%d,%d", &l, &rr, &k) == 3 && apk::pick_r2(l, rr, k, dense) && rr > 0 &&
         w % rr == 0 && w / rr <= uint32_t(l)) {
+      const uint32_t ring = apk::ring_slots(W, 2 * apk::kChunk, l);
       out->L = l; out->R = 2 * rr; out->K = k; out->xm = false; out->r2 = true; out->ring = ring;
       out->smem = apk::kWarpsPerCta *
                   apk::comb_smem_per_warp(l, k * apk::r2_band_words(rr / k), sigma_y, ring, 2 * apk::kChunk);
@@ -175,6 +176,7 @@ bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
       continue;
     }
     const int bw = apk::r2_band_words(d.RR / d.K);
+    const uint32_t ring = apk::ring_slots(W, 2 * apk::kChunk, d.L);
     const size_t smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(d.L, d.K * bw, sigma_y, ring, 2 * apk::kChunk);
     if (smem > kSmemPerSm - 1024) continue;
     const int by_regs = 65536 / (std::max(fa.numRegs, 1) * 32 * apk::kWarpsPerCta);

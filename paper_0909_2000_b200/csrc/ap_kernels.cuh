@@ -103,11 +103,15 @@ __host__ __device__ constexpr int ring_stride(int L, int nb) { return L * ((nb +
 // strip B, so a slot reads back as the packed pair oA | oB << 16) plus 32 bytes
 // of padding so the same slot of different groups falls 8 banks apart.
 __host__ __device__ constexpr size_t ok_stride(uint32_t ring) { return size_t(4) * ring + 32; }
-// ring slots the extraction needs: the W + NB starts between the oldest unread
-// flag and the newest bottom column, plus the clear-ahead window of NB + 31
-// (extract_body); a power of two
-__host__ __device__ constexpr uint32_t ring_slots(uint32_t W, int nb) {
-  uint32_t need = W + 2 * uint32_t(nb) + 31, r = 128;
+// ring slots the extraction needs (extract_body): the W + NB + A starts between
+// the oldest unread flag and the end of the clear-ahead window, with the
+// clear-ahead offset A = NB (+ (-W) mod CPL when lane runs are CPL-aligned, i.e.
+// L divides 32 and NB); a power of two >= 128
+__host__ __device__ constexpr uint32_t ring_slots(uint32_t W, int nb, int L) {
+  const bool align = 32 % L == 0 && nb % L == 0;
+  const uint32_t cpl = uint32_t((nb + L - 1) / L);
+  const uint32_t need = W + 2 * uint32_t(nb) + (align ? (cpl - W % cpl) % cpl : 0u);
+  uint32_t r = 128;
   while (r < need) r <<= 1;
   return r;
 }
@@ -223,7 +227,7 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
 //    Those starts cannot have exited yet (A >= NB), so the stray flags of the
 //    chunk (all aimed inside this range) are wiped before the slot is used,
 //    and no per-seaweed select or branch is needed.  Live slots span
-//    W + NB + A <= W + 2 NB + 31 starts (ring_slots).
+//    W + NB + A starts (ring_slots).
 //  * When L divides 32 and NB, slots are offset by delta so that every lane's
 //    run of CPL read slots and CPL cleared slots is CPL-aligned: one vector
 //    load / store per lane and no per-column wrap masks.
