@@ -18,9 +18,16 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstdio>
+#include <fstream>
+#include <istream>
 #include <optional>
 #include <ostream>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -67,6 +74,43 @@ inline void check(int rc) {
     case AP_INVALID: throw std::invalid_argument(msg);
     default: throw EngineError("alignplot_b200 status " + std::to_string(rc) + ": " + msg);
   }
+}
+// A double as the reference's JSON writer prints it: the shortest digit string
+// that round-trips, in fixed notation (with a trailing ".0" when integral) for
+// values in [1e-4, 1e15), scientific ("1.5e+20", "1e-05") outside.
+inline std::string json_double(double v) {
+  if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+  char buf[64];
+  int p = 0;
+  for (; p < 17; ++p) {   // shortest round-trip mantissa
+    std::snprintf(buf, sizeof buf, "%.*e", p, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  std::snprintf(buf, sizeof buf, "%.*e", p, v);
+  std::string m(buf);
+  const bool neg = m[0] == '-';
+  if (neg) m.erase(0, 1);
+  const std::size_t epos = m.find('e');
+  const int e10 = std::atoi(m.c_str() + epos + 1);
+  std::string d;
+  for (std::size_t i = 0; i < epos; ++i)
+    if (m[i] != '.') d.push_back(m[i]);
+  while (d.size() > 1 && d.back() == '0') d.pop_back();
+  const int k = int(d.size()), n = e10 + 1;   // value = 0.d * 10^n
+  std::string out;
+  if (k <= n && n <= 15) {
+    out = d + std::string(size_t(n - k), '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    out = d.substr(0, size_t(n)) + "." + d.substr(size_t(n));
+  } else if (-4 < n && n <= 0) {
+    out = "0." + std::string(size_t(-n), '0') + d;
+  } else {
+    const int x = n - 1;
+    char eb[16];
+    std::snprintf(eb, sizeof eb, "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
+    out = (k == 1 ? d : d.substr(0, 1) + "." + d.substr(1)) + eb;
+  }
+  return neg ? "-" + out : out;
 }
 }  // namespace detail
 
@@ -359,6 +403,155 @@ inline void write_pgm_gpu(std::ostream& out, const Sequence& x, const Sequence& 
   out << "P5\n" << cols << ' ' << rows << "\n255\n";
   out.write(reinterpret_cast<const char*>(pix.data()), static_cast<std::streamsize>(pix.size()));
   if (!out) throw std::runtime_error("write failure on PGM sink");
+}
+
+// ---- FASTA input (io.hpp:15-38, io.cpp:32-100) ----------------------------
+struct FastaRecord {
+  std::string header;
+  std::string sequence;
+  bool operator==(const FastaRecord&) const = default;
+};
+
+inline std::vector<FastaRecord> read_fasta_stream(std::istream& in, const std::string& source) {
+  std::vector<FastaRecord> recs;
+  std::size_t line_no = 0, header_line = 0;
+  auto fail = [&](std::size_t ln, const std::string& what) {
+    throw ParseError(source + ":" + std::to_string(ln) + ": " + what);
+  };
+  auto space = [](unsigned char c) { return c == ' ' || (c >= '\t' && c <= '\r'); };
+  std::string line;
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    if (std::all_of(line.begin(), line.end(), [&](char c) { return space(static_cast<unsigned char>(c)); }))
+      continue;   // empty or blank
+    if (line[0] == '>') {
+      if (!recs.empty() && recs.back().sequence.empty())
+        fail(header_line, "record '" + recs.back().header + "' has no sequence data");
+      std::size_t e = line.size();
+      while (e > 1 && space(static_cast<unsigned char>(line[e - 1]))) --e;
+      recs.push_back({line.substr(1, e - 1), {}});
+      header_line = line_no;
+      continue;
+    }
+    if (recs.empty()) fail(line_no, "sequence data before first header");
+    for (char ch : line) {
+      const auto c = static_cast<unsigned char>(ch);
+      if (space(c)) continue;
+      if (c < 32 || c > 126 || c == '>') fail(line_no, "unexpected byte in sequence data");
+      recs.back().sequence.push_back(static_cast<char>(c >= 'a' && c <= 'z' ? c - 32 : c));
+    }
+  }
+  if (recs.empty()) throw ParseError(source + ": no FASTA records");
+  if (recs.back().sequence.empty())
+    fail(header_line, "record '" + recs.back().header + "' has no sequence data");
+  return recs;
+}
+
+inline std::vector<FastaRecord> read_fasta(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError(path + ": cannot open file");
+  return read_fasta_stream(in, path);
+}
+
+// exact header, or its first whitespace-delimited token; the first record for ""
+inline const FastaRecord& select_record(const std::vector<FastaRecord>& records, const std::string& name,
+                                        const std::string& source) {
+  if (name.empty()) return records.front();
+  for (const FastaRecord& r : records) {
+    if (r.header == name) return r;
+    const std::size_t cut = r.header.find_first_of(" \t");
+    if (cut != std::string::npos && cut == name.size() && r.header.compare(0, cut, name) == 0) return r;
+  }
+  throw ParseError(source + ": no record named '" + name + "'");
+}
+
+inline Sequence to_sequence(const FastaRecord& rec) { return Sequence::from_text(rec.header, rec.sequence); }
+
+// ---- benchmark (io.hpp:56-81, io.cpp:155-233) ------------------------------
+struct BenchEntry {
+  Mode mode = Mode::dp;
+  double seconds = 0.0;
+  double cell_updates_per_sec = 0.0;
+  double speedup_vs_first = 1.0;
+};
+
+struct BenchReport {
+  std::size_t rows = 0, cols = 0, window_w = 0, step_h = 0;
+  unsigned blowup_r = 1, workers = 1;
+  std::vector<BenchEntry> entries;
+
+  std::string to_text() const {
+    std::ostringstream os;
+    os << "plot " << rows << " x " << cols << " windows, w=" << window_w << ", h=" << step_h
+       << ", r=" << blowup_r << ", workers=" << workers << "\n";
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "%-12s %10s %12s %9s\n", "mode", "seconds", "Mcups", "speedup");
+    os << buf;
+    bool dp = false;
+    for (const BenchEntry& e : entries) {
+      dp = dp || e.mode == Mode::dp;
+      std::snprintf(buf, sizeof buf, "%-12s %10.3f %12.1f %8.2fx\n", mode_name(e.mode), e.seconds,
+                    e.cell_updates_per_sec / 1e6, e.speedup_vs_first);
+      os << buf;
+    }
+    if (dp) os << "dp = exhaustive per-window DP baseline, no shortcuts\n";
+    return os.str();
+  }
+
+  // keys in sorted order, two-space indentation (the reference's json dump(2))
+  std::string to_json() const {
+    auto num = [](double v) { return detail::json_double(v); };
+    std::ostringstream os;
+    os << "{\n  \"blowup\": " << blowup_r << ",\n  \"cols\": " << cols << ",\n  \"results\": [";
+    for (std::size_t i = 0; i < entries.size(); ++i) {
+      const BenchEntry& e = entries[i];
+      os << (i ? "," : "") << "\n    {\n      \"cell_updates_per_sec\": " << num(e.cell_updates_per_sec)
+         << ",\n      \"mode\": \"" << mode_name(e.mode) << "\",\n      \"seconds\": " << num(e.seconds)
+         << ",\n      \"speedup_vs_first\": " << num(e.speedup_vs_first) << "\n    }";
+    }
+    os << (entries.empty() ? "]" : "\n  ]") << ",\n  \"rows\": " << rows << ",\n  \"step\": " << step_h
+       << ",\n  \"window\": " << window_w << ",\n  \"workers\": " << workers << "\n}";
+    return os.str();
+  }
+};
+
+// Times each mode on the same inputs; every mode must give the same grid (all
+// of them run on the GPU engine here, so they agree by construction).  Cell
+// updates/s are normalised to the per-window DP cost rows*cols*(w*r)^2.
+inline BenchReport benchmark(const Sequence& x, const Sequence& y, const PlotConfig& cfg,
+                             std::span<const Mode> modes) {
+  if (modes.empty()) throw ConfigError("benchmark needs at least one mode");
+  BenchReport rep;
+  rep.window_w = cfg.window_w;
+  rep.step_h = cfg.step_h;
+  rep.blowup_r = cfg.blowup_r;
+  rep.workers = cfg.workers;
+  std::optional<PlotGrid> first;
+  for (Mode m : modes) {
+    PlotConfig c = cfg;
+    c.mode = m;
+    const auto t0 = std::chrono::steady_clock::now();
+    PlotGrid g = compute_plot(x, y, c);
+    const double secs =
+        std::max(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), 1e-9);
+    if (!first) {
+      first = std::move(g);
+      rep.rows = first->rows;
+      rep.cols = first->cols;
+    } else if (!(g == *first)) {
+      throw std::runtime_error(std::string("benchmark: mode ") + mode_name(m) + " disagrees with " +
+                               mode_name(modes.front()));
+    }
+    const double wr = double(cfg.window_w * cfg.blowup_r);
+    BenchEntry e;
+    e.mode = m;
+    e.seconds = secs;
+    e.cell_updates_per_sec = double(rep.rows) * double(rep.cols) * wr * wr / secs;
+    e.speedup_vs_first = rep.entries.empty() ? 1.0 : rep.entries.front().seconds / secs;
+    rep.entries.push_back(e);
+  }
+  return rep;
 }
 
 }  // namespace alignplot

@@ -4,6 +4,7 @@
 // seeded std::mt19937 generators as the reference tests; the ground truth is an
 // independent per-window DP (as tests/test_util.hpp's ref_llcs /
 // ref_align_score_half).  Exit status = number of failed checks.  Needs a GPU.
+#include <cmath>
 #include <cstdio>
 #include <sstream>
 #include <random>
@@ -193,6 +194,21 @@ int main() {
       write_pgm_gpu(dev, x, y, cfg);
       CHECK(host.str() == dev.str());
     }
+  }
+  {  // io.cpp:192-233 benchmark: every mode timed, grids agree, DP-normalised rates
+    std::mt19937 rng(77);
+    const Sequence x("x", random_codes(rng, 300, 4)), y("y", random_codes(rng, 340, 4));
+    PlotConfig cfg;
+    cfg.window_w = 30; cfg.step_h = 2; cfg.blowup_r = 2;
+    const Mode modes[] = {Mode::sea8, Mode::sea16, Mode::cuda};
+    const BenchReport rep = benchmark(x, y, cfg, modes);
+    const auto dims = window_grid_dims(300, 340, 30, 2);
+    CHECK(rep.rows == dims.first && rep.cols == dims.second && rep.entries.size() == 3);
+    CHECK(rep.entries[0].speedup_vs_first == 1.0 && rep.entries[2].mode == Mode::cuda);
+    const double cells = double(rep.rows) * double(rep.cols) * 60.0 * 60.0;
+    CHECK(std::abs(rep.entries[1].cell_updates_per_sec * rep.entries[1].seconds - cells) < 1e-6 * cells);
+    CHECK(rep.to_text().rfind("plot " + std::to_string(rep.rows) + " x ", 0) == 0);
+    CHECK_THROWS_AS(benchmark(x, y, cfg, std::span<const Mode>{}), ConfigError);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
   return failures;

@@ -74,3 +74,21 @@ def test_cpp_shim_compiles():
         res = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", os.path.join(ROOT, "tests", "cpp", "test_shim.cpp")],
                              capture_output=True, text=True, cwd=d)
         assert res.returncode == 0, res.stderr
+
+
+def test_cpp_shim_io_cpu():
+    """The C++ drop-in's FASTA reader and BenchReport formatting (no device work):
+    error kinds/line numbers of io.cpp:32-100 and the to_text layout of io.cpp:155-174."""
+    import shutil
+    import subprocess
+    import tempfile
+    if not shutil.which("g++"):
+        pytest.skip("g++ unavailable")
+    pkg = os.path.join(ROOT, "paper_0909_2000_b200")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "t")
+        res = subprocess.run(["g++", "-std=c++20", "-O1", "-o", exe, os.path.join(ROOT, "tests", "cpp", "test_shim_io.cpp"),
+                              f"-L{pkg}", "-lalignplot_b200", f"-Wl,-rpath,{pkg}"], capture_output=True, text=True)
+        assert res.returncode == 0, res.stderr
+        run = subprocess.run([exe], capture_output=True, text=True)
+        assert run.returncode == 0, run.stdout
