@@ -143,6 +143,13 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 #ifndef AP_FMAMIN_RR
 #define AP_FMAMIN_RR 4   // r = 2 kernels with RR >= this compute one mismatch min with IMADs (C4: -1.3%)
 #endif
+#ifndef AP_SUBUNROLL
+#define AP_SUBUNROLL 2   // generic kernel: unroll of the 8-step sub loop (4 per chunk; C5 -3%)
+#endif
+constexpr int kSubUnroll = AP_SUBUNROLL;
+#ifndef AP_SUBUNROLL2_RR
+#define AP_SUBUNROLL2_RR 4  // r = 2 kernel: shapes with RR <= this unroll all 4 subs of a chunk (C4 -7%; C2 +4%)
+#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -635,7 +642,7 @@ comb_kernel(const CombParams p) {
     uint32_t nsub = 0;
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
-#pragma unroll 1
+#pragma unroll kSubUnroll
       for (int sub = 0; sub < kChunk / 8; ++sub, ++nsub) {
         const uint4 na = __ldg(yq + 2 * nsub + 4), nb = __ldg(yq + 2 * nsub + 5);
         uint32_t* ring_sub = ringB + sub * 8;
@@ -771,6 +778,7 @@ comb2_kernel(const CombParams p) {
   constexpr int BW = r2_band_words(RRB);
   constexpr int Q4 = RRB / 4, REM = RRB % 4;
   constexpr int NB = 2 * kChunk;   // blown bottom columns per chunk
+  constexpr int kSubUnroll2 = RR <= AP_SUBUNROLL2_RR ? kChunk / 8 : 1;
   constexpr bool kFmaMin = RR >= AP_FMAMIN_RR;  // one of the two mismatch mins moves to the FMA pipe
   extern __shared__ __align__(16) unsigned char smem[];
 
@@ -869,7 +877,7 @@ comb2_kernel(const CombParams p) {
     for (uint32_t ch = 0; ch < nch; ++ch) {
       const uint4 nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
       const uint4 nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
-#pragma unroll 1
+#pragma unroll kSubUnroll2
       for (int sub = 0; sub < kChunk / 8; ++sub) {
         const uint32_t w0 = sub == 0 ? ych.x : sub == 1 ? ych.z : sub == 2 ? ych2.x : ych2.z;
         const uint32_t w1 = sub == 0 ? ych.y : sub == 1 ? ych.w : sub == 2 ? ych2.y : ych2.w;
