@@ -122,7 +122,9 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
       if (ctas < 1) continue;
       const int warps = ctas * apk::kWarpsPerCta;
       double cost = double(d.L) * ((xm ? 6.0 : 3.0) * d.R + 14.0) + 25.0;
-      if (warps < 16) cost *= 16.0 / warps;
+      // long lanes (R = 32) hide latency with ILP: only penalise below 8 warps per SM
+      // (B200: comb<8,32,4> at 8 warps beats comb<16,16,4> at 16 warps on C5 by 3%)
+      if (warps < 8) cost *= 8.0 / warps;
       cost *= d.K == 4 ? 0.95 : 1.0;   // 4 bands: more ILP per lane (measured ~5% faster)
       if (cost < best) {
         best = cost;
