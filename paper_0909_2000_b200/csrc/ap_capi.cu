@@ -55,6 +55,7 @@ using apk::KernelFn;
 // Instantiated shapes: (L lanes per strip pair, R rows per lane, K bands per lane).
 struct ShapeDef { int L, R, K; };
 constexpr ShapeDef kShapes[] = {
+    {4, 32, 2}, {4, 32, 4},
     {8, 8, 2},  {8, 16, 2},  {8, 16, 4},  {8, 24, 2},  {8, 32, 2},  {8, 32, 4},
     {16, 8, 2}, {16, 16, 2}, {16, 16, 4}, {16, 24, 2}, {16, 32, 2}, {16, 32, 4},
     {32, 8, 2}, {32, 16, 2}, {32, 16, 4}, {32, 24, 2}, {32, 32, 2}, {32, 32, 4},
@@ -62,6 +63,7 @@ constexpr ShapeDef kShapes[] = {
 
 KernelFn pick_kernel(int l, int r, int k, bool dense, bool xm) {
   switch (l) {
+    case 4: return apk::pick_l4(r, k, dense, xm);
     case 8: return apk::pick_l8(r, k, dense, xm);
     case 16: return apk::pick_l16(r, k, dense, xm);
     case 32: return apk::pick_l32(r, k, dense, xm);
@@ -125,7 +127,8 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
       // long lanes (R = 32) hide latency with ILP: only penalise below 8 warps per SM
       // (B200: comb<8,32,4> at 8 warps beats comb<16,16,4> at 16 warps on C5 by 3%)
       if (warps < 8) cost *= 8.0 / warps;
-      cost *= d.K == 4 ? 0.95 : 1.0;   // 4 bands: more ILP per lane (measured ~5% faster)
+      cost *= d.K == 4 && d.L >= 8 ? 0.95 : 1.0;   // 4 bands: more ILP per lane (measured ~5% faster)
+      // (L = 4: comb<4,32,2> beats comb<4,32,4> and comb<8,16,4> on C3 by 2-5% on B200)
       if (cost < best) {
         best = cost;
         out->L = d.L;

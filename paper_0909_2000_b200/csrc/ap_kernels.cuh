@@ -83,6 +83,7 @@ struct CombParams {
 
 using KernelFn = void (*)(CombParams);
 // Launch-stub pointers of the instantiated comb kernels (ap_inst_l{8,16,32}.cu).
+KernelFn pick_l4(int r, int k, bool dense, bool xm);
 KernelFn pick_l8(int r, int k, bool dense, bool xm);
 KernelFn pick_l16(int r, int k, bool dense, bool xm);
 KernelFn pick_l32(int r, int k, bool dense, bool xm);
@@ -207,6 +208,7 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
                                                      int nb = kChunk) {
   const int Ga = groups_alloc(L);
   const size_t bytes = size_t(4) * 32 * sigma * table_words   // mismatch table (sigma = 0: computed masks)
+       + (sigma && L < 8 ? size_t(32 / L) * 64 : 0)            // L < 8: groups 64 B apart (bank halves)
        + ((size_t(Ga) * ring_stride(L, nb) * 4 + 15) & ~size_t(15))   // bottom-key ring per group (padded)
        + size_t(32 / L) * ok_stride(ring)                      // ok flags per group (strip A, strip B)
        + (Ga > 32 / L ? 64 : 0);                               // phantom group: ring mask 0, 64-B scratch
@@ -529,7 +531,7 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 template <int L, int R, int K, bool DENSE, bool XM>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
-  static_assert(32 % L == 0 && L >= 8, "table layout needs L >= 8 (conflict-free LDS.128)");
+  static_assert(32 % L == 0 && L >= 4, "lane groups must tile the warp");
   static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
   constexpr int G = 32 / L;
   constexpr int Q = R / 4;        // quads per lane
@@ -545,9 +547,13 @@ comb_kernel(const CombParams p) {
   const uint32_t j = lane % L;
   const size_t per_warp = comb_smem_per_warp(L, R, p.sigma, p.ring);
   unsigned char* wbase = smem + warp * per_warp;
-  uint4* tbl = reinterpret_cast<uint4*>(wbase);                       // [G][sigma][Q][L]
-  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + size_t(128) * p.sigma * R) + g * (kChunk + 1);
-  const uint32_t okb = uint32_t(__cvta_generic_to_shared(wbase + size_t(128) * p.sigma * R)) +
+  uint4* tbl = reinterpret_cast<uint4*>(wbase);                       // [G][sigma][Q][L] (+pad)
+  // group stride of the table in uint4: with L < 8 a group's LDS.128 covers only
+  // 64 B, so consecutive groups are shifted by 64 B to use the other bank half
+  const size_t tgs = size_t(p.sigma) * Q * L + (L < 8 && p.sigma ? 4 : 0);
+  const size_t tbytes = size_t(G) * tgs * 16;
+  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbytes) + g * (kChunk + 1);
+  const uint32_t okb = uint32_t(__cvta_generic_to_shared(wbase + tbytes)) +
                        ((G * (kChunk + 1) * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
   const uint32_t rshift = p.r - 1;
 
@@ -595,7 +601,7 @@ comb_kernel(const CombParams p) {
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) xpair[rho] = xa[rho] | (xb[rho] << 16);
       } else {
-        uint4* tg = tbl + size_t(g) * p.sigma * Q * L;
+        uint4* tg = tbl + size_t(g) * tgs;
         for (uint32_t a = 0; a < p.sigma; ++a) {
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
@@ -614,7 +620,7 @@ comb_kernel(const CombParams p) {
     __syncwarp();
 
     // table base of this lane; y column words are byte offsets of a code's quads
-    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + size_t(g) * p.sigma * Q * L + j));
+    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + size_t(g) * tgs + j));
     const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
     // lane-select constants: the band-0 inputs are imad(shuffled, nz, own) on the
     // FMA pipe instead of selects (own = fresh key / new column word on lane 0, 0 elsewhere)

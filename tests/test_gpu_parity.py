@@ -184,7 +184,7 @@ def test_cli_matches_reference_cli_bytes():
         assert out.stdout == want, case["name"]
 
 
-@pytest.mark.parametrize("shape", ["8,8,2", "8,16,2", "8,16,4", "16,16,4", "32,8,2", "32,32,4", "16,24,2"])
+@pytest.mark.parametrize("shape", ["4,32,2", "4,32,4", "8,8,2", "8,16,2", "8,16,4", "16,16,4", "32,8,2", "32,32,4", "16,24,2"])
 def test_forced_generic_shapes(shape, monkeypatch):
     """Every instantiated generic (L, R, K) shape, forced with AP_SHAPE, is bit-exact."""
     monkeypatch.setenv("AP_SHAPE", shape)
@@ -281,7 +281,7 @@ def test_long_sequences_dense_and_threshold(w, r, h, sigma):
         assert np.array_equal(gh, want[rr, cc]), t
 
 
-@pytest.mark.parametrize("shape", ["8,16,4", "16,8,2", "32,8,2"])
+@pytest.mark.parametrize("shape", ["4,32,4", "8,16,4", "16,8,2", "32,8,2"])
 def test_forced_generic_shapes_long_y(shape, monkeypatch):
     """Forced generic shapes on a y long enough for interior chunks and rebases, both r."""
     monkeypatch.setenv("AP_SHAPE", shape)
