@@ -532,6 +532,7 @@ template <int L, int R, int K, bool DENSE, bool XM>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
   static_assert(32 % L == 0 && L >= 4, "lane groups must tile the warp");
+  constexpr int kSU = L < 8 ? 1 : kSubUnroll;   // L = 4 (R = 32): the bigger body runs best rolled
   static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
   constexpr int G = 32 / L;
   constexpr int Q = R / 4;        // quads per lane
@@ -648,7 +649,7 @@ comb_kernel(const CombParams p) {
     uint32_t nsub = 0;
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
-#pragma unroll kSubUnroll
+#pragma unroll kSU
       for (int sub = 0; sub < kChunk / 8; ++sub, ++nsub) {
         const uint4 na = __ldg(yq + 2 * nsub + 4), nb = __ldg(yq + 2 * nsub + 5);
         uint32_t* ring_sub = ringB + sub * 8;
