@@ -184,17 +184,20 @@ def test_cli_matches_reference_cli_bytes():
         assert out.stdout == want, case["name"]
 
 
-@pytest.mark.parametrize("shape", ["4,32,2", "4,32,4", "8,8,2", "8,16,2", "8,16,4", "16,16,4", "32,8,2", "32,32,4", "16,24,2"])
+@pytest.mark.parametrize("shape", ["4,32,2", "4,32,4", "8,8,2", "8,16,2", "8,16,4", "16,16,4", "32,8,2", "32,32,4",
+                                   "16,24,2", "4,32,2,1", "8,16,4,1", "16,16,4,1"])
 def test_forced_generic_shapes(shape, monkeypatch):
-    """Every instantiated generic (L, R, K) shape, forced with AP_SHAPE, is bit-exact."""
+    """Every instantiated generic (L, R, K) shape, forced with AP_SHAPE, is bit-exact
+    (",1" = the computed-mask variant, exercised with a 60-letter alphabet)."""
     monkeypatch.setenv("AP_SHAPE", shape)
     monkeypatch.setenv("AP_NO_R2", "1")
-    rng = np.random.default_rng(hash(shape) & 0xFFFF)
-    L, R, K = map(int, shape.split(","))
+    rng = np.random.default_rng(sum(map(ord, shape)))
+    L, R, K = map(int, shape.split(",")[:3])
+    sigma = 60 if shape.count(",") == 3 else 4
     for r in (1, 2):
         w = max(2, min((L * R) // r - 3, 200))
-        x = rng.integers(1, 5, w + 150).astype(np.uint8)
-        y = rng.integers(1, 5, w + 700).astype(np.uint8)
+        x = rng.integers(1, sigma + 1, w + 150).astype(np.uint8)
+        y = rng.integers(1, sigma + 1, w + 700).astype(np.uint8)
         rc, want = ol.plot_rows(x, y, w, 2, r)
         assert np.array_equal(gpu_grid(x, y, w, 2, r), want), (shape, r)
 
