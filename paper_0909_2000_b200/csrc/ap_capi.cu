@@ -83,6 +83,7 @@ struct Shape {
   int L = 0, R = 0, K = 2;
   bool r2 = false;   // r = 2 specialised kernel (comb2_kernel); R = 2*RR then
   bool xm = false;   // masks computed in registers (no table)
+  bool hf = false;   // r = 2 kernel with fp16 keys (one mismatch min on the FMA pipe)
   uint32_t ring = 0;
   size_t smem = 0;
   int warps_per_sm = 0;
@@ -157,23 +158,29 @@ constexpr Shape2Def kShapes2[] = {
 bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
   if (std::getenv("AP_NO_R2")) return false;
   const uint32_t W = 2 * w;
-  // tuning override: AP_SHAPE2="L,RR,K"
+  // fp16 keys need W + 2*VB <= kHfMaxSpan (VB = virtual bands down the strip)
+  auto hf_ok = [&](int rr, int k) { return W + 2 * (w / uint32_t(rr)) * uint32_t(k) <= apk::kHfMaxSpan; };
+  // tuning override: AP_SHAPE2="L,RR,K[,hf]" (hf: 0/1, default: the automatic choice)
   if (const char* env = std::getenv("AP_SHAPE2")) {
-    int l = 0, rr = 0, k = 0;
-    if (std::sscanf(env, "%d,%d,%d", &l, &rr, &k) == 3 && apk::pick_r2(l, rr, k, dense) && rr > 0 &&
-        w % rr == 0 && w / rr <= uint32_t(l)) {
+    int l = 0, rr = 0, k = 0, hf = -1;
+    const int nf = std::sscanf(env, "%d,%d,%d,%d", &l, &rr, &k, &hf);
+    if (nf >= 3 && rr > 0 && w % rr == 0 && w / rr <= uint32_t(l)) {
+      if (hf < 0) hf = apk::pick_r2(l, rr, k, dense, true) && hf_ok(rr, k);
+      if ((!hf || hf_ok(rr, k)) && apk::pick_r2(l, rr, k, dense, hf)) {
       const uint32_t ring = apk::ring_slots(W, 2 * apk::kChunk, l);
-      out->L = l; out->R = 2 * rr; out->K = k; out->xm = false; out->r2 = true; out->ring = ring;
+      out->L = l; out->R = 2 * rr; out->K = k; out->xm = false; out->r2 = true; out->hf = hf; out->ring = ring;
       out->smem = apk::kWarpsPerCta *
                   apk::comb_smem_per_warp(l, k * apk::r2_band_words(rr / k), sigma_y, ring, 2 * apk::kChunk);
       out->warps_per_sm = 0;
       return out->smem <= kSmemPerSm - 1024;
+      }
     }
   }
   double best = 1e30;
   for (const Shape2Def& d : kShapes2) {
     if (w % d.RR || w / d.RR > uint32_t(d.L)) continue;
-    KernelFn fn = apk::pick_r2(d.L, d.RR, d.K, dense);
+    const bool hf = apk::pick_r2(d.L, d.RR, d.K, dense, true) && hf_ok(d.RR, d.K);
+    KernelFn fn = apk::pick_r2(d.L, d.RR, d.K, dense, hf);
     if (!fn) continue;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)) != cudaSuccess) {
@@ -202,6 +209,7 @@ bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
       out->K = d.K;
       out->xm = false;
       out->r2 = true;
+      out->hf = hf;
       out->ring = ring;
       out->smem = smem;
       out->warps_per_sm = warps;
@@ -375,7 +383,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh))
       return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                   sigma, W);
-    plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense)
+    plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf)
                         : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm);
     if (!plan.fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", plan.sh.L, plan.sh.R);
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),

@@ -16,17 +16,18 @@
 // the same grid-row pair share every y character).  Left-boundary seaweeds
 // have key 0 (they start left of everything, seaweed_scalar.cpp:21-22).  The
 // cell rule "exchange iff match or start(V) > start(T)"
-// (seaweed_scalar.cpp:26-32) becomes, with NF = 0 on a match and all-ones on a
-// mismatch (per 16-bit half):
-//     d      = max_u16x2(V, T & NF)      // seaweed leaving downwards
-//     V'     = V ^ T ^ d                 // seaweed leaving to the right
-// i.e. LOP3 + VIMNMX.U16x2 + LOP3 for two cells: no increment, no saturation
-// in the inner loop.  Keys are rebased (saturating at 0) every ~32K columns;
-// a rebased-to-0 seaweed is provably older than any window.
+// (seaweed_scalar.cpp:26-32) becomes, with A = 0x8000 (-32768 as s16) on a
+// match and 0 on a mismatch (per 16-bit half):
+//     d      = max_s16x2(T + A, V)       // seaweed leaving downwards (VIADDMNMX)
+//     V'     = V ^ T ^ d                 // seaweed leaving to the right (LOP3)
+// i.e. two ALU instructions for two cells: no increment, no saturation in the
+// inner loop.  Keys stay in [0, 0x7BFF] and are rebased (saturating at 0) every
+// ~28K columns; a rebased-to-0 seaweed is provably older than any window
+// (DESIGN.md §3).
 //
-// NF comes from a per-warp shared-memory table indexed by the y code: the
+// A comes from a per-warp shared-memory table indexed by the y code: the
 // x-window characters are fixed for a strip, so table[code][row] holds the
-// mismatch mask of both strips; one LDS.128 serves four rows.
+// match words of both strips; one LDS.128 serves four rows.
 //
 // Mapping.  A warp holds 32/L groups; a group of L lanes combs one strip pair,
 // lane j owning R consecutive rows [j*R, j*R+R).  Lane j processes column
@@ -88,7 +89,7 @@ KernelFn pick_l8(int r, int k, bool dense, bool xm);
 KernelFn pick_l16(int r, int k, bool dense, bool xm);
 KernelFn pick_l32(int r, int k, bool dense, bool xm);
 // The r = 2 specialised kernels (ap_inst_r2.cu): RR real rows per lane.
-KernelFn pick_r2(int l, int rr, int k, bool dense);
+KernelFn pick_r2(int l, int rr, int k, bool dense, bool hf = false);
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -151,6 +152,20 @@ constexpr int kSubUnroll = AP_SUBUNROLL;
 #ifndef AP_SUBUNROLL2_RR
 #define AP_SUBUNROLL2_RR 4  // r = 2 kernel: shapes with RR <= this unroll all 4 subs of a chunk (C4 -7%; C2 +4%)
 #endif
+// fp16 key encoding (r = 2 kernels with HF = true): live keys are 0x6400 + k =
+// the fp16 value 1024 + k (k < 1024), left-boundary keys 0 (+0.0).  The integer
+// order of the patterns is the order of the values, so the integer min/max cells
+// are unchanged, and min(v, t) = (v - max(v, t)) + t is exact in fp16 (every
+// intermediate is an integer of magnitude < 2048): one mismatch min per row
+// moves to the FMA pipe as two 2-operand HADD2s (C2: 6.25 -> 6.06 ms on B200;
+// slower than the IMAD form for RR = 4 shapes, so only RR >= 8 use it).
+// Keys are rebased every ~hf_by columns (W + 2*VB <= kHfMaxSpan, host-checked).
+constexpr uint32_t kHfBase = 0x6400u;
+constexpr uint32_t kHfRebaseAt = 0x6400u + 0x3C0u;   // fresh keys stay < 0x6400 + 1024
+constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: rebase step >= 128 columns
+#ifndef AP_R2_ROWMAJOR
+#define AP_R2_ROWMAJOR 0   // 1: r = 2 step row pair by row pair (fewer $-row swap moves; B200: C2 +0.6%, C4 +0.7%)
+#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -191,6 +206,18 @@ __device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// fp16x2 add / subtract (round to nearest: exact on the key encoding below)
+__device__ __forceinline__ uint32_t hadd2u(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hsub2u(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
 
@@ -775,7 +802,7 @@ __device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t*
   }
 }
 
-template <int L, int RR, int K, bool DENSE>
+template <int L, int RR, int K, bool DENSE, bool HF>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= AP_R2_MB4 ? 4 : (RR <= 16 ? 3 : 2))
 comb2_kernel(const CombParams p) {
   static_assert(L <= 32 && RR % K == 0, "bad shape");
@@ -873,8 +900,11 @@ comb2_kernel(const CombParams p) {
     uint32_t tbD[K], tbR[K], cd[K];
 #pragma unroll
     for (int b = 0; b < K; ++b) { tbD[b] = 0u; tbR[b] = 0u; cd[b] = 0u; }
-    int32_t kbase = -int32_t(p.W) - 1;
+    int32_t kbase = -int32_t(p.W) - 1 - (HF ? int32_t(kHfBase) : 0);
     uint32_t fresh = uint32_t(-kbase) * 0x00010001u;   // key of blown column 2s
+    // rebase step: with the fp16 encoding as large as keeps every seaweed that a
+    // later window can count (starts >= the next chunk's E0 - W + 1)
+    const uint32_t rebase_by = HF ? (kHfRebaseAt - kHfBase - 2 * kChunk - 2 * VB - p.W) & ~1u : kRebaseBy;
     uint32_t run = 0u, hitsA = 0u, hitsB = 0u;
 
     uint4 ych = __ldg(reinterpret_cast<const uint4*>(yw));
@@ -908,6 +938,37 @@ comb2_kernel(const CombParams p) {
             for (int b = 1; b < K; ++b) { tinD[b] = tbD[b - 1]; tinR[b] = tbR[b - 1]; }
           }
           fresh += 0x00020002u;
+#if AP_R2_ROWMAJOR
+          // Row pair by row pair, both blown columns at once.  $ row 2i: the
+          // ($,$) swap sends the old V down column 2c and takes column 2c's
+          // seaweed, which then meets column 2c+1's (never a match): down =
+          // max, V = min.  Real row 2i+1: ($ col) max/min, then (real, real).
+          // The old $-row V is consumed before its new value is written, so
+          // every V keeps its register across steps (no swap moves).
+#pragma unroll
+          for (int b = 0; b < K; ++b) {
+            uint32_t tD = tinD[b], tR = tinR[b];
+#pragma unroll
+            for (int i = 0; i < RRB; ++i) {
+              uint32_t& vs = V[b * 2 * RRB + 2 * i];
+              uint32_t& vr = V[b * 2 * RRB + 2 * i + 1];
+              const uint32_t dD = vs;                          // down column 2c
+              const uint32_t dR = __vmaxu2(tD, tR);            // down column 2c+1
+              uint32_t nvs;
+              if constexpr (kFmaMin) nvs = imad(dR, p.minus_one, imad(tD, p.one, tR));   // min = tD + tR - max
+              else nvs = __vminu2(tD, tR);
+              const uint32_t eD = __vmaxu2(vr, dD);
+              const uint32_t vr1 = __vminu2(vr, dD);
+              const uint32_t eR = __viaddmax_s16x2(dR, m[b][i], vr1);
+              vr = lop3_xor(vr1, dR, eR);
+              vs = nvs;
+              tD = eD;
+              tR = eR;
+            }
+            tbD[b] = tD;
+            tbR[b] = tR;
+          }
+#else
 #pragma unroll
           for (int b = 0; b < K; ++b) {
             uint32_t t = tinD[b];                       // blown column 2c: $
@@ -928,7 +989,9 @@ comb2_kernel(const CombParams p) {
             for (int i = 0; i < RRB; ++i) {
               uint32_t& vs = V[b * 2 * RRB + 2 * i];     // $ row: mismatch
               const uint32_t d0 = __vmaxu2(vs, t);
-              if constexpr (kFmaMin) {
+              if constexpr (HF) {
+                vs = hadd2u(hsub2u(vs, d0), t);   // fp16: (vs - max) + t = min, exact
+              } else if constexpr (kFmaMin) {
                 // min(vs, t) = vs + t - max(vs, t) as two IMADs on the otherwise idle
                 // FMA pipe (16-bit halves never carry): unloads the ALU pipe, which
                 // this kernel saturates at RR >= 8 (C2: 7.27 -> 6.95 ms on B200)
@@ -946,6 +1009,7 @@ comb2_kernel(const CombParams p) {
             }
             tbR[b] = t;
           }
+#endif
           if (j == lanes_real - 1) {
             ring_sub[2 * u] = tbD[K - 1];
             ring_sub[2 * u + 1] = tbR[K - 1];
@@ -966,17 +1030,18 @@ comb2_kernel(const CombParams p) {
       extract_chunk<L, NB, DENSE>(p, ringB, okb, okmask, j, g, lane,
                                   2 * (int32_t(ch * kChunk) - int32_t(VB - 1)), nseg_cols, kbase, c0, rA,
                                   rB, hasA, hasB, run, hitsA, hitsB);
-      if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= kRebaseAt) {
-        const uint32_t by = kRebaseBy * 0x00010001u;
+      if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= (HF ? kHfRebaseAt : kRebaseAt)) {
+        const uint32_t by = rebase_by * 0x00010001u;
+        const uint32_t fl = (HF ? kHfBase : 0u) * 0x00010001u + by;   // saturated keys -> the floor
 #pragma unroll
-        for (int i = 0; i < R; ++i) V[i] = __vmaxu2(V[i], by) - by;
+        for (int i = 0; i < R; ++i) V[i] = __vmaxu2(V[i], fl) - by;
 #pragma unroll
         for (int b = 0; b < K; ++b) {
-          tbD[b] = __vmaxu2(tbD[b], by) - by;
-          tbR[b] = __vmaxu2(tbR[b], by) - by;
+          tbD[b] = __vmaxu2(tbD[b], fl) - by;
+          tbR[b] = __vmaxu2(tbR[b], fl) - by;
         }
         fresh -= by;
-        kbase += int32_t(kRebaseBy);
+        kbase += int32_t(rebase_by);
       }
     }
     if constexpr (!DENSE) {

@@ -202,12 +202,19 @@ def test_forced_generic_shapes(shape, monkeypatch):
         assert np.array_equal(gpu_grid(x, y, w, 2, r), want), (shape, r)
 
 
-@pytest.mark.parametrize("shape", ["4,25,5", "4,25,1", "10,10,2", "10,10,1", "5,20,4", "5,20,1", "8,8,2",
-                                   "16,4,2", "32,4,2", "16,10,2", "8,20,4", "32,5,1"])
+R2_SHAPES = ["4,25,5", "4,25,1", "10,10,2", "10,10,1", "5,20,4", "5,20,1", "8,8,2", "8,8,4", "16,8,4",
+             "32,8,4", "8,16,4", "16,16,4", "32,16,4", "16,4,2", "32,4,2", "16,10,2", "8,20,4", "32,5,1",
+             "32,4,1", "16,4,1"]
+
+
+@pytest.mark.parametrize("shape", [s + ",0" for s in R2_SHAPES] +
+                         [s + ",1" for s in R2_SHAPES if int(s.split(",")[1]) >= 8])
 def test_forced_r2_shapes(shape, monkeypatch):
-    """Every instantiated r = 2 (L, RR, K) shape, forced with AP_SHAPE2, is bit-exact (dense and threshold)."""
+    """Every instantiated r = 2 (L, RR, K) shape, forced with AP_SHAPE2, is bit-exact (dense and
+    threshold), with integer keys (,0) and -- for the RR >= 8 shapes -- fp16 keys (,1; rebased
+    every few hundred columns, so these short strips already cross several rebases)."""
     monkeypatch.setenv("AP_SHAPE2", shape)
-    L, RR, K = map(int, shape.split(","))
+    L, RR, K, _ = map(int, shape.split(","))
     w = RR * min(L, max(1, 100 // RR))
     rng = np.random.default_rng(RR * 131 + L)
     x = rng.integers(1, 5, w + 120).astype(np.uint8)
@@ -215,6 +222,22 @@ def test_forced_r2_shapes(shape, monkeypatch):
     rc, want = ol.plot_rows(x, y, w, 1, 2)
     assert np.array_equal(gpu_grid(x, y, w, 1, 2), want), shape
     t = int(np.quantile(want, 0.95))
+    rr, cc = np.nonzero(want >= t)
+    gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
+    assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape
+
+
+@pytest.mark.parametrize("shape,w", [("32,16,4,1", 288), ("16,10,2,1", 160), ("10,10,2,1", 100)])
+def test_forced_r2_fp16_keys_long(shape, w, monkeypatch):
+    """fp16-key r = 2 kernel at the largest span it accepts (w = 288: W + 2*VB = 720, rebased
+    every 176 blown columns) and at C2's shape, over a long y with planted homology."""
+    monkeypatch.setenv("AP_SHAPE2", shape)
+    rng = np.random.default_rng(w)
+    x = rng.integers(1, 5, w + 90).astype(np.uint8)
+    y = np.concatenate([rng.integers(1, 5, 1500), x[20:w + 60], rng.integers(1, 5, 2500)]).astype(np.uint8)
+    rc, want = ol.plot_rows(x, y, w, 1, 2)
+    assert np.array_equal(gpu_grid(x, y, w, 1, 2), want), shape
+    t = int(want.max()) - 6
     rr, cc = np.nonzero(want >= t)
     gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape

@@ -16,6 +16,11 @@ __device__ __forceinline__ uint32_t lop3x(uint32_t a, uint32_t b, uint32_t c) {
 __device__ __forceinline__ uint32_t vam(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d; asm volatile("{.reg .b32 t; add.s16x2 t, %1, %2; max.s16x2 %0, t, %3;}" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
 
+__device__ __forceinline__ uint32_t hadd2x(uint32_t a, uint32_t b) {
+  uint32_t d; asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t hsub2x(uint32_t a, uint32_t b) {
+  uint32_t d; asm volatile("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+
 // NCH chains, each RB cells deep per step; V[NCH*RB] state, M[NCH*RB] masks (registers)
 template <int NCH, int RB, int VAR>
 __global__ void k_cell(uint32_t* out, Rec* rec, uint32_t seed) {
@@ -40,6 +45,18 @@ __global__ void k_cell(uint32_t* out, Rec* rec, uint32_t seed) {
         } else if constexpr (VAR == 1) {    // same, LOP3 operand order t first (reuse of t)
           const uint32_t d = __viaddmax_s16x2(t, M[c * RB + k], v);
           v = lop3x(t, v, d);
+          t = d;
+        } else if constexpr (VAR >= 3 && VAR <= 6) {
+          // V' = (V - d) + T as fp16 values (keys 0x6400 + k = 1024 + k: exact), on the FMA pipe,
+          // for the first F rows of each group of 4 (F = 4, 2, 3, 1 for VAR 3..6)
+          constexpr int F = VAR == 3 ? 4 : VAR == 4 ? 2 : VAR == 5 ? 3 : 1;
+          const uint32_t d = __viaddmax_s16x2(t, M[c * RB + k], v);
+          if ((k & 3) < F) v = hadd2x(hsub2x(v, d), t);
+          else v = lop3x(v, t, d);
+          t = d;
+        } else if constexpr (VAR == 7) {    // max + fp16 (v - d) + t
+          const uint32_t d = __vmaxu2(v, t);
+          v = hadd2x(hsub2x(v, d), t);
           t = d;
         } else {                            // mismatch-only comparator: max + min (2-operand ops)
           const uint32_t d = __vmaxu2(v, t);
@@ -89,6 +106,11 @@ int main() {
     run(k_cell<8, 2, 0>, "viaddmax+lop3 8x2", w, 16);
     run(k_cell<2, 8, 0>, "viaddmax+lop3 2x8", w, 16);
     run(k_cell<4, 4, 2>, "vmax+vmin 4x4", w, 16);
+    run(k_cell<4, 4, 3>, "viaddmax+hsub2+hadd2 (all rows) 4x4", w, 16);
+    run(k_cell<4, 4, 4>, "viaddmax + 2/4 rows hadd2, 2/4 lop3 4x4", w, 16);
+    run(k_cell<4, 4, 5>, "viaddmax + 3/4 rows hadd2, 1/4 lop3 4x4", w, 16);
+    run(k_cell<4, 4, 6>, "viaddmax + 1/4 rows hadd2, 3/4 lop3 4x4", w, 16);
+    run(k_cell<4, 4, 7>, "vmax + hsub2+hadd2 4x4", w, 16);
   }
   return 0;
 }
