@@ -61,7 +61,8 @@ constexpr ShapeDef kShapes[] = {
     {32, 8, 2}, {32, 16, 2}, {32, 16, 4}, {32, 24, 2}, {32, 32, 2}, {32, 32, 4},
 };
 
-KernelFn pick_kernel(int l, int r, int k, bool dense, bool xm) {
+KernelFn pick_kernel(int l, int r, int k, bool dense, bool xm, bool hf = false) {
+  if (hf) return xm ? nullptr : apk::pick_ghf(l, r, k, dense);
   switch (l) {
     case 4: return apk::pick_l4(r, k, dense, xm);
     case 8: return apk::pick_l8(r, k, dense, xm);
@@ -70,6 +71,9 @@ KernelFn pick_kernel(int l, int r, int k, bool dense, bool xm) {
   }
   return nullptr;
 }
+
+// fp16 keys (HF kernels) need the rebase step to stay >= 128 columns
+bool ghf_ok(uint32_t W, int l, int k) { return W + uint32_t(l * k) <= apk::kHfMaxSpan; }
 
 constexpr size_t kSmemPerSm = 227 * 1024;
 
@@ -83,7 +87,7 @@ struct Shape {
   int L = 0, R = 0, K = 2;
   bool r2 = false;   // r = 2 specialised kernel (comb2_kernel); R = 2*RR then
   bool xm = false;   // masks computed in registers (no table)
-  bool hf = false;   // r = 2 kernel with fp16 keys (one mismatch min on the FMA pipe)
+  bool hf = false;   // fp16 keys: one cell op per row (r = 2: a mismatch min; generic: V' of one row in 4) on the FMA pipe
   uint32_t ring = 0;
   size_t smem = 0;
   int warps_per_sm = 0;
@@ -93,13 +97,14 @@ struct Shape {
 // masks] + ~14 per-step overhead) + ~25 extraction ops, scaled up when fewer than
 // 16 warps per SM fit (registers from the compiled kernel, table in shared memory).
 bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
-  // tuning override: AP_SHAPE="L,R,K[,xm]"
+  // tuning override: AP_SHAPE="L,R,K[,xm[,hf]]" (hf default: the automatic choice)
   if (const char* env = std::getenv("AP_SHAPE")) {
-    int l = 0, r = 0, k = 0, xm = 0;
-    if (std::sscanf(env, "%d,%d,%d,%d", &l, &r, &k, &xm) >= 3 && pick_kernel(l, r, k, dense, xm) &&
-        uint32_t(l * r) >= W) {
+    int l = 0, r = 0, k = 0, xm = 0, hf = -1;
+    const int nf = std::sscanf(env, "%d,%d,%d,%d,%d", &l, &r, &k, &xm, &hf);
+    if (hf < 0) hf = !xm && ghf_ok(W, l, k) && pick_kernel(l, r, k, dense, false, true);
+    if (nf >= 3 && (!hf || ghf_ok(W, l, k)) && pick_kernel(l, r, k, dense, xm, hf) && uint32_t(l * r) >= W) {
       const uint32_t ring = apk::ring_slots(W, apk::kChunk, l);
-      out->L = l; out->R = r; out->K = k; out->xm = xm; out->ring = ring;
+      out->L = l; out->R = r; out->K = k; out->xm = xm; out->hf = hf; out->ring = ring;
       out->smem = apk::kWarpsPerCta * apk::comb_smem_per_warp(l, r, xm ? 0 : sigma, ring);
       out->warps_per_sm = 0;
       return out->smem <= kSmemPerSm - 1024;
@@ -109,7 +114,8 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
   for (int xm = 0; xm < 2; ++xm) {
     for (const ShapeDef& d : kShapes) {
       if (uint32_t(d.L * d.R) < W) continue;
-      KernelFn fn = pick_kernel(d.L, d.R, d.K, dense, xm);
+      const bool hf = !xm && ghf_ok(W, d.L, d.K) && pick_kernel(d.L, d.R, d.K, dense, false, true);
+      KernelFn fn = pick_kernel(d.L, d.R, d.K, dense, xm, hf);
       if (!fn) continue;
       cudaFuncAttributes fa;
       if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)) != cudaSuccess) {
@@ -136,6 +142,7 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
         out->R = d.R;
         out->K = d.K;
         out->xm = xm;
+        out->hf = hf;
         out->ring = ring;
         out->smem = smem;
         out->warps_per_sm = warps;
@@ -384,7 +391,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                   sigma, W);
     plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf)
-                        : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm);
+                        : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm, plan.sh.hf);
     if (!plan.fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", plan.sh.L, plan.sh.R);
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.sh.smem)));

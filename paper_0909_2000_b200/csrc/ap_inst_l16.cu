@@ -7,8 +7,8 @@ namespace apk {
 
 template <int R, int K>
 static KernelFn pick(bool dense, bool xm) {
-  if (dense) return xm ? &comb_kernel<16, R, K, true, true> : &comb_kernel<16, R, K, true, false>;
-  return xm ? &comb_kernel<16, R, K, false, true> : &comb_kernel<16, R, K, false, false>;
+  if (dense) return xm ? &comb_kernel<16, R, K, true, true, false> : &comb_kernel<16, R, K, true, false, false>;
+  return xm ? &comb_kernel<16, R, K, false, true, false> : &comb_kernel<16, R, K, false, false, false>;
 }
 
 KernelFn pick_l16(int r, int k, bool dense, bool xm) {

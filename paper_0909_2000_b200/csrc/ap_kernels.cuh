@@ -88,6 +88,8 @@ KernelFn pick_l4(int r, int k, bool dense, bool xm);
 KernelFn pick_l8(int r, int k, bool dense, bool xm);
 KernelFn pick_l16(int r, int k, bool dense, bool xm);
 KernelFn pick_l32(int r, int k, bool dense, bool xm);
+// fp16-key variants (table masks only; W + L*K <= kHfMaxSpan): ap_inst_ghf_{a,b}.cu
+KernelFn pick_ghf(int l, int r, int k, bool dense);
 // The r = 2 specialised kernels (ap_inst_r2.cu): RR real rows per lane.
 KernelFn pick_r2(int l, int rr, int k, bool dense, bool hf = false);
 
@@ -158,8 +160,10 @@ constexpr int kSubUnroll = AP_SUBUNROLL;
 // are unchanged, and min(v, t) = (v - max(v, t)) + t is exact in fp16 (every
 // intermediate is an integer of magnitude < 2048): one mismatch min per row
 // moves to the FMA pipe as two 2-operand HADD2s (C2: 6.25 -> 6.06 ms on B200;
-// slower than the IMAD form for RR = 4 shapes, so only RR >= 8 use it).
-// Keys are rebased every ~hf_by columns (W + 2*VB <= kHfMaxSpan, host-checked).
+// slower than the IMAD form for RR = 4 shapes, so only RR >= 8 use it).  The
+// generic kernel with HF = true computes V' = (V - d) + T (two HADD2s) instead
+// of the LOP3 for one row of every four (C3 -1.2%, C5 -2%; two rows: slower).
+// Keys are rebased every rebase_by columns (W + 2*VB <= kHfMaxSpan, host-checked).
 constexpr uint32_t kHfBase = 0x6400u;
 constexpr uint32_t kHfRebaseAt = 0x6400u + 0x3C0u;   // fresh keys stay < 0x6400 + 1024
 constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: rebase step >= 128 columns
@@ -555,9 +559,10 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 // XM = true (any alphabet): A computed from the x-code pair registers:
 //   A = ~((xpair ^ y * 0x10001) + 0x7FFF7FFF) & 0x80008000 (bit 15 of a half
 //   survives iff the codes are equal).
-template <int L, int R, int K, bool DENSE, bool XM>
+template <int L, int R, int K, bool DENSE, bool XM, bool HF>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
+  constexpr int kHfRows = HF ? 1 : 0;   // rows of each quad whose V' is formed on the FMA pipe
   static_assert(32 % L == 0 && L >= 4, "lane groups must tile the warp");
   constexpr int kSU = L < 8 ? 1 : kSubUnroll;   // L = 4 (R = 32): the bigger body runs best rolled
   static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
@@ -662,8 +667,9 @@ comb_kernel(const CombParams p) {
     uint32_t cd[K];     // y column word of band b at the current step
 #pragma unroll
     for (int b = 0; b < K; ++b) { tb[b] = 0u; cd[b] = 0u; }
-    int32_t kbase = -int32_t(p.W) - 1;                 // key(c) = c - kbase > W for top seaweeds
+    int32_t kbase = -int32_t(p.W) - 1 - (HF ? int32_t(kHfBase) : 0);   // key(c) = c - kbase > W for top seaweeds
     uint32_t fresh = j == 0 ? uint32_t(-kbase) * 0x00010001u : 0u;   // key of column s, both halves
+    const uint32_t rebase_by = HF ? (kHfRebaseAt - kHfBase - 2 * kChunk - VB - p.W) : kRebaseBy;
     const uint32_t one = p.one;
     const uint32_t tblmul = kTblMul * one;   // opaque: keeps IMAD.HI (FMA pipe), not LEA.HI (ALU)
     uint32_t run = 0u;
@@ -719,7 +725,8 @@ comb_kernel(const CombParams p) {
               for (int k = 0; k < 4; ++k) {
                 uint32_t& v = V[b * RB + 4 * qq + k];
                 const uint32_t d = __viaddmax_s16x2(t, m[k], v);   // max(T + A, V): A = -32768 on a match
-                v = lop3_xor(v, t, d);
+                if (k < kHfRows) v = hadd2u(hsub2u(v, d), t);   // fp16 keys: V + T - d, exact
+                else v = lop3_xor(v, t, d);
                 t = d;
               }
             }
@@ -745,14 +752,15 @@ comb_kernel(const CombParams p) {
                                       hasA, hasB, run, hitsA, hitsB);
 
       // ---- key rebase (saturating at 0): fresh keys stay below 0x7BFF (fp16-finite)
-      if (uint32_t(int32_t((ch + 2) * kChunk) - kbase) >= kRebaseAt) {
-        const uint32_t by = kRebaseBy * 0x00010001u;
+      if (uint32_t(int32_t((ch + 2) * kChunk) - kbase) >= (HF ? kHfRebaseAt : kRebaseAt)) {
+        const uint32_t by = rebase_by * 0x00010001u;
+        const uint32_t fl = (HF ? kHfBase : 0u) * 0x00010001u + by;   // saturated keys -> the floor
 #pragma unroll
-        for (int rho = 0; rho < R; ++rho) V[rho] = __vmaxu2(V[rho], by) - by;
+        for (int rho = 0; rho < R; ++rho) V[rho] = __vmaxu2(V[rho], fl) - by;
 #pragma unroll
-        for (int b = 0; b < K; ++b) tb[b] = __vmaxu2(tb[b], by) - by;
+        for (int b = 0; b < K; ++b) tb[b] = __vmaxu2(tb[b], fl) - by;
         if (j == 0) fresh -= by;
-        kbase += int32_t(kRebaseBy);
+        kbase += int32_t(rebase_by);
       }
     }
     if constexpr (!DENSE) {

@@ -184,11 +184,17 @@ def test_cli_matches_reference_cli_bytes():
         assert out.stdout == want, case["name"]
 
 
-@pytest.mark.parametrize("shape", ["4,32,2", "4,32,4", "8,8,2", "8,16,2", "8,16,4", "16,16,4", "32,8,2", "32,32,4",
-                                   "16,24,2", "4,32,2,1", "8,16,4,1", "16,16,4,1"])
+GENERIC_SHAPES = ["4,32,2", "4,32,4", "8,8,2", "8,16,2", "8,16,4", "8,24,2", "8,32,2", "8,32,4", "16,8,2",
+                  "16,16,2", "16,16,4", "16,24,2", "16,32,2", "16,32,4", "32,8,2", "32,16,2", "32,16,4",
+                  "32,24,2", "32,32,2", "32,32,4"]
+
+
+@pytest.mark.parametrize("shape", [s + ",0,0" for s in GENERIC_SHAPES] + [s + ",0,1" for s in GENERIC_SHAPES] +
+                         ["4,32,2,1", "8,16,4,1", "16,16,4,1", "32,8,2,1"])
 def test_forced_generic_shapes(shape, monkeypatch):
-    """Every instantiated generic (L, R, K) shape, forced with AP_SHAPE, is bit-exact
-    (",1" = the computed-mask variant, exercised with a 60-letter alphabet)."""
+    """Every instantiated generic (L, R, K) shape, forced with AP_SHAPE, is bit-exact:
+    table masks with integer keys (",0,0") and with fp16 keys (",0,1"), and the
+    computed-mask variant (",1", exercised with a 60-letter alphabet)."""
     monkeypatch.setenv("AP_SHAPE", shape)
     monkeypatch.setenv("AP_NO_R2", "1")
     rng = np.random.default_rng(sum(map(ord, shape)))
@@ -240,6 +246,23 @@ def test_forced_r2_fp16_keys_long(shape, w, monkeypatch):
     t = int(want.max()) - 6
     rr, cc = np.nonzero(want >= t)
     gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
+    assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape
+
+
+@pytest.mark.parametrize("shape,w,r", [("32,32,2,0,1", 640, 1), ("16,16,4,0,1", 256, 1), ("8,32,2,0,1", 120, 2)])
+def test_forced_generic_fp16_keys_long(shape, w, r, monkeypatch):
+    """fp16-key generic kernel at the largest span it accepts (w = 640: W + L*K = 704, rebased
+    every 192 columns), at C5's shape and in r = 2 mode, over a long y with planted homology."""
+    monkeypatch.setenv("AP_SHAPE", shape)
+    monkeypatch.setenv("AP_NO_R2", "1")
+    rng = np.random.default_rng(w + r)
+    x = rng.integers(1, 5, w + 70).astype(np.uint8)
+    y = np.concatenate([rng.integers(1, 5, 1200), x[30:w + 50], rng.integers(1, 5, 2200)]).astype(np.uint8)
+    rc, want = ol.plot_rows(x, y, w, 1, r)
+    assert np.array_equal(gpu_grid(x, y, w, 1, r), want), shape
+    t = int(want.max()) - 6
+    rr, cc = np.nonzero(want >= t)
+    gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape
 
 
