@@ -135,6 +135,19 @@ def workload(name: str, world: int):
     return c, x, y
 
 
+def kernel_ceiling(kernel: str, peak_ops_clk: float):
+    """Comb cells per SM clock at which the chosen kernel saturates the ALU pipe (cells count
+    both strips of a packed u32).  Generic kernel per u32 = one cell of each of two strips:
+    VIADDMNMX + LOP3 (2 ALU ops); fp16 keys move one row in four's LOP3 to two HADD2s on the
+    FMA pipe (1.75); computed masks add LOP3 + IADD + LOP3 (5).  r = 2 kernel per u32 block of
+    2 x 2 blown cells x two strips: 3 VIMNMX + VIADDMNMX + LOP3 (5 ALU ops; the ($,$) swap is
+    free, the other mismatch min runs on the FMA pipe as two IMADs or two HADD2s)."""
+    if kernel.startswith("comb2"):
+        return peak_ops_clk * 8.0 / 5.0, "r=2 kernel: 5 ALU ops per 8 blown cells"
+    ops = 5.0 if ",computed," in kernel else (1.75 if kernel.endswith("fp16>") else 2.0)
+    return peak_ops_clk * 2.0 / ops, f"generic kernel {kernel}: {ops:g} ALU ops per 2 cells"
+
+
 def comb_cells(rows, c, n):
     return rows * (c.w * c.r) * (n * c.r)
 
@@ -281,7 +294,7 @@ def run_engine(args, rank, world, local_rank):
         dist.barrier()
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kern_ms, launches = [], 0
+    kern_ms, launches, kernel = [], 0, ""
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -293,6 +306,7 @@ def run_engine(args, rank, world, local_rank):
             evs[i][1].record(stream)
             evs[i][1].synchronize()   # so the comb-kernel events of this step can be read
             kern_ms.append(L.ap_ctx_last_kernel_ms(ctx))
+            kernel = (L.ap_ctx_last_kernel(ctx) or b"").decode()
             launches += L.ap_ctx_last_launches(ctx)
         torch.cuda.synchronize()
         if world > 1:
@@ -306,6 +320,14 @@ def run_engine(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max, kern_max = float(t[0]), float(t[1])
     hits_local = int(count.value) if not dense else 0
+    # thresholded output: the one collective of the path, a gather of per-rank hit counts (the
+    # exclusive prefix of it places each rank's row-major list in the global one)
+    hits_all = [hits_local]
+    if world > 1 and not dense:
+        cnt_t = torch.tensor([hits_local], dtype=torch.int64, device=red_dev)
+        gathered = [torch.zeros_like(cnt_t) for _ in range(world)]
+        dist.all_gather(gathered, cnt_t)
+        hits_all = [int(g_.item()) for g_ in gathered]
 
     # ---- end to end through the public host API (pinned host buffers) ----
     hx = torch.from_numpy(xs.copy()).pin_memory()
@@ -388,17 +410,13 @@ def run_engine(args, rank, world, local_rank):
             with open(NCU_TRAFFIC) as f:
                 traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
         cpc = cells_local / kern_max / (props.multi_processor_count * sm_mhz * 1e6)
-        # generic kernel: VIADDMNMX + LOP3 per u32 (two strips x one cell) on the ALU pipe
-        #   -> peak_ops_clk cells/clk/SM;
-        # r = 2 kernel: per u32 block of two strips x (2 x 2 blown cells) 5 ALU ops (3 VIMNMX,
-        #   VIADDMNMX, LOP3; the $ x $ swap is free) + 2 IMAD -> 8 * peak_ops_clk / 5 cells/clk/SM
-        ceiling = peak_ops_clk * (8.0 / 5.0 if c.r == 2 else 1.0)
+        ceiling, ceiling_what = kernel_ceiling(kernel, peak_ops_clk)
         roof = {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel_alu_bound": {"cells_per_clk_per_sm": cpc, "ceiling": ceiling, "frac": cpc / ceiling,
-                                     "what": "comb cells per SM clock vs this kernel's own instruction ceiling "
-                                             "(ALU pipe at the measured rate; r=1: 2 ALU ops per 2 cells (one u32 = two strips); "
-                                             "r=2: 5 ALU ops per 8 blown cells)"},
+                "kernel_alu_bound": {"kernel": kernel, "cells_per_clk_per_sm": cpc, "ceiling": ceiling,
+                                     "frac": cpc / ceiling,
+                                     "what": "comb cells per SM clock vs this kernel's own ALU-pipe instruction "
+                                             "ceiling at the measured rate: " + ceiling_what},
                 "basis": "3 int32 lane-ops per comb cell (SURVEY §8d), cells = rows*(w*r)*(n*r); peak = "
                          f"{props.multi_processor_count} SMs x {peak_ops_clk:.1f} measured lane-ops/clk/SM x "
                          f"{sm_mhz:.0f} MHz (median SM clock during the run)",
@@ -431,10 +449,12 @@ def run_engine(args, rank, world, local_rank):
         "e2e": {"value": wpcu * args.steps / t_e2e, "unit": "window-pair cell updates/s",
                 "h2d_bytes_per_step": int(xs.size + n), "d2h_bytes_per_step": int(d2h)},
         "e2e_compact": e2e_u8,
-        "gpu_launches": launches, "cpu_baseline": cpu,
+        "gpu_launches": launches, "kernel": kernel, "cpu_baseline": cpu,
     }
     if not dense:
         line["hits_rank0"] = hits_local
+        line["hits_total"] = sum(hits_all)
+        line["hits_per_rank"] = hits_all
     print(json.dumps(line), flush=True)
     L.ap_ctx_destroy(ctx)
 

@@ -150,6 +150,11 @@ float ap_ctx_last_kernel_ms(ap_ctx* ctx);
 /* Number of kernel launches the last call on ctx enqueued. */
 int ap_ctx_last_launches(ap_ctx* ctx);
 
+/* The comb kernel the last call on ctx chose, e.g. "comb2<10,10,2,fp16>" or
+ * "comb<4,32,2,table,fp16>" (lanes per strip pair, rows per lane, bands; mask
+ * source; key encoding); "" before the first call.  Valid until the next call. */
+const char* ap_ctx_last_kernel(ap_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

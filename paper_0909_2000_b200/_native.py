@@ -26,7 +26,7 @@ EXPORTS = (
     "ap_last_error",
     "ap_device_count", "ap_ctx_create", "ap_ctx_destroy", "ap_ctx_plot_dense_device",
     "ap_ctx_plot_threshold_device", "ap_ctx_plot_pgm_device", "ap_ctx_plot_dense_u8_device",
-    "ap_ctx_last_kernel_ms", "ap_ctx_last_launches",
+    "ap_ctx_last_kernel_ms", "ap_ctx_last_launches", "ap_ctx_last_kernel",
 )
 
 
@@ -103,6 +103,8 @@ def lib() -> ctypes.CDLL:
     L.ap_ctx_last_kernel_ms.restype = c_float
     L.ap_ctx_last_launches.argtypes = [c_void_p]
     L.ap_ctx_last_launches.restype = c_int
+    L.ap_ctx_last_kernel.argtypes = [c_void_p]
+    L.ap_ctx_last_kernel.restype = c_char_p
     _lib = L
     return L
 

@@ -271,6 +271,7 @@ struct ap_ctx {
   size_t cap_orow = 0, cap_ocol = 0, cap_ohalf = 0;
   float last_ms = 0.f;
   int last_launches = 0;
+  char last_kernel[64] = "";
 };
 
 namespace {
@@ -402,6 +403,12 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   }
   const Shape& sh = plan.sh;
   const bool spec = plan.spec;
+  if (spec)
+    std::snprintf(c->last_kernel, sizeof(c->last_kernel), "comb2<%d,%d,%d,%s>", sh.L, sh.R / 2, sh.K,
+                  sh.hf ? "fp16" : "int");
+  else
+    std::snprintf(c->last_kernel, sizeof(c->last_kernel), "comb<%d,%d,%d,%s,%s>", sh.L, sh.R, sh.K,
+                  sh.xm ? "computed" : "table", sh.hf ? "fp16" : "int");
   // the dynamic-smem limit is a per-function attribute and other plans may have
   // lowered it since this plan was cached
   CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),
@@ -687,6 +694,8 @@ float ap_ctx_last_kernel_ms(ap_ctx* c) {
 }
 
 int ap_ctx_last_launches(ap_ctx* c) { return c ? c->last_launches : 0; }
+
+const char* ap_ctx_last_kernel(ap_ctx* c) { return c ? c->last_kernel : ""; }
 
 int ap_ctx_plot_dense_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
                              const ap_config* cfg, uint16_t* d_out, void* stream) {
