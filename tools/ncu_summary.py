@@ -29,9 +29,21 @@ def main():
     for r in rows[1:]:
         if len(r) > vi and r[ni] in KEYS:
             print(f"  {r[ni]}: {r[vi]} {r[ui]}")
-    for r in rows[1:]:
-        if len(r) > vi and r[ni] == "" and "stall" in "".join(r).lower():
-            pass
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    if len(rr) > 2:
+        d = dict(zip(rr[0], rr[2]))
+        pipes = [("ALU", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                 ("FMA", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                 ("issue", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                 ("LSU shared wavefronts", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")]
+        print("  pipes (% of peak):", ", ".join(f"{n} {float(d[k]):.1f}" for n, k in pipes if d.get(k)))
+        pre = "smsp__pcsamp_warps_issue_stalled_"
+        st = {k[len(pre):]: float(v.replace(",", "")) for k, v in d.items()
+              if k.startswith(pre) and not k.endswith("_not_issued") and v.replace(",", "").replace(".", "").isdigit()}
+        tot_st = sum(st.values()) or 1.0
+        print("  warp states (pc samples):", ", ".join(f"{k} {v / tot_st:.3f}"
+                                                     for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:9]))
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))

@@ -1,21 +1,25 @@
 #!/bin/bash
 # Round measurement bundle (run under gpurun):  tools/profile_round.sh r01
-#   1. bench.py default (C2) plain run            -> gpurun_out/$R/bench_C2.json
-#   2. ncu launch list of the same command         -> gpurun_out/$R/launches_C2.csv
-#   3. ncu --set full of the top kernel (C2 rows)  -> gpurun_out/$R/prof_C2.ncu-rep
-#   4. other configs' bench lines                  -> gpurun_out/$R/bench_C{1,3,4}.json
+#   bench lines (all five configs, CPU reference sample beside each), the reference arm,
+#   the ncu launch list of the default bench (C2), and ncu --set full of the comb kernel
+#   per config (full grid for C1/C2, a row block for C3-C5)            -> gpurun_out/$R/
 R=${1:-r01}
 O=gpurun_out/$R
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt 2>&1
 python bench.py > $O/bench_C2.json 2> $O/bench_C2.err
+python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_C2_reference.json 2> $O/bench_C2_reference.err
+python bench.py --config C1 > $O/bench_C1.json 2> $O/bench_C1.err
+python bench.py --config C3 --steps 5 --warmup 3 > $O/bench_C3.json 2> $O/bench_C3.err
+python bench.py --config C4 --steps 3 --warmup 3 > $O/bench_C4.json 2> $O/bench_C4.err
+python bench.py --config C5 --steps 1 --warmup 3 > $O/bench_C5.json 2> $O/bench_C5.err
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/plain_small.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2.csv \
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
-python tools/prof_step.py --config C2 --rows 16285 --reps 1 > $O/prof_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:comb -c 1 -o $O/prof_C2 \
-      python tools/prof_step.py --config C2 --rows 16285 --reps 1 > $O/ncu_full.log 2>&1
-for c in C1 C3 C4; do
-  python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
+for cr in C1:0 C2:0 C3:8192 C4:4096 C5:512; do
+  c=${cr%%:*}; n=${cr##*:}
+  python tools/prof_step.py --config $c --rows $n --reps 1 > $O/prof_$c.log 2>&1 && \
+    ncu --set full --clock-control none --import-source on -k regex:comb -c 1 -o $O/prof_$c \
+        python tools/prof_step.py --config $c --rows $n --reps 1 > $O/ncu_full_$c.log 2>&1
 done
 ls -la $O
