@@ -77,11 +77,6 @@ bool ghf_ok(uint32_t W, int l, int k) { return W + uint32_t(l * k) <= apk::kHfMa
 
 constexpr size_t kSmemPerSm = 227 * 1024;
 
-uint32_t next_pow2(uint32_t v) {
-  uint32_t p = 1;
-  while (p < v) p <<= 1;
-  return p;
-}
 
 struct Shape {
   int L = 0, R = 0, K = 2;
@@ -242,11 +237,12 @@ struct ap_ctx {
   std::map<uint64_t, LaunchPlan> plans;   // cached per (w, r, sigma, dense) and env overrides
   cudaStream_t stream = nullptr;
   cudaStream_t stream_copy = nullptr;   // D2H of finished row blocks (overlaps the comb kernel)
-  cudaStream_t stream_b = nullptr;      // second compute stream: consecutive row blocks overlap
+  cudaStream_t stream_b = nullptr;      // second compute stream (compute-bound streamed plots)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   static constexpr int kMaxBlocks = 32;
   cudaEvent_t ev_blk[kMaxBlocks] = {};
-  cudaEvent_t ev_aux[2] = {};
+  cudaEvent_t ev_cp[kMaxBlocks] = {};   // copy-done events (AP_TRACE timelines)
+  cudaEvent_t ev_join = nullptr;
   std::mutex mu;
   // scratch (grown on demand)
   uint8_t *d_x = nullptr, *d_y = nullptr, *d_xcode = nullptr, *d_ycode = nullptr, *d_map = nullptr;
@@ -352,6 +348,10 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
 // at d_x (already offset to the first row).  dense: writes d_out.
 // out_kind (dense only): 0 = uint16 half-units into d_out, 1 = uint8 PGM pixels
 // (io.cpp:136-153 fused; cfg->has_threshold renders cells below it black).
+#ifndef AP_STREAM_GROWTH
+#define AP_STREAM_GROWTH 1.3
+#endif
+
 int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
                const ap_config* cfg, size_t nrows, size_t row_global0, bool dense,
                void* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
@@ -506,45 +506,86 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   CK(cudaEventRecord(c->ev0, st));
   if (dense && host_out) {
-    // Dense output to the host: launch the plot as ~16 row blocks alternating
-    // over two compute streams (consecutive blocks overlap, so small blocks do
-    // not leave the GPU idle) and stream every finished block's D2H on the copy
-    // stream, so the PCIe transfer hides under the comb kernels of later blocks.
-    // blocks of at least half a wave each (two run concurrently), at most 16
-    const size_t nblk = std::min<size_t>({std::max<size_t>(ntasks / std::max<size_t>(total_warps / 2, 1), 1),
-                                          std::max<size_t>(ngroups, 1), 16});
-    const size_t gpb = (ngroups + nblk - 1) / nblk;          // pair groups per block
+    // Dense output to the host: the plot streams out row block by row block while later
+    // blocks comb (copy stream), so the end-to-end time is about max(comb, D2H) plus the
+    // exposed ends.  The comb costs ~0.057 ps per blown cell, the D2H (PCIe, ~57 GB/s)
+    // ~17.5 ps per byte on B200:
+    //  * D2H-bound (uint16 output, W*r < ~600; C2): e2e = (time to the first finished
+    //    block) + D2H + ~50 us per copy.  Short tasks (segments of ~max(2048, 8W) columns:
+    //    ~0.4 ms per task on C2 instead of ~1.3 ms) on one stream, in row blocks of
+    //    round(1.3^k) full waves (equal tasks, so a block ends without a ragged tail; a
+    //    block's comb fits in the previous block's D2H, so the copy engine never idles):
+    //    the first copy starts after one task time, with ~8 copies in all.
+    //  * compute-bound (1-byte output): normal segments, ~16 equal row blocks of at least
+    //    half a wave alternating over two compute streams (consecutive blocks overlap), so
+    //    only the last block's copy is exposed.
     const size_t elem = out_kind == 0 ? 2 : 1;
-    CK(cudaEventRecord(c->ev_aux[0], st));                   // code streams ready
-    CK(cudaStreamWaitEvent(c->stream_b, c->ev_aux[0], 0));
-    size_t launched = 0;
+    const bool d2h_bound = double(elem) * 17.5 > 0.057 * double(W) * double(r);
+    size_t Ss = d2h_bound ? std::max<size_t>(2048, 8 * size_t(W)) : S;
+    Ss = std::min(Ss, S);
+    Ss = std::max<size_t>((Ss + salign - 1) / salign * salign, salign);
+    const size_t nseg_s = (out_cols_eff + Ss - 1) / Ss;
+    size_t blk_g0[ap_ctx::kMaxBlocks + 1];
+    size_t nblk = 0;
+    if (d2h_bound) {
+      const size_t wave_groups = std::max<size_t>(1, total_warps / nseg_s);   // pair groups per wave
+      size_t g = 0;
+      double waves = 1.0;
+      while (g < ngroups && nblk < size_t(ap_ctx::kMaxBlocks)) {
+        blk_g0[nblk++] = g;
+        const size_t wk = std::max<size_t>(1, size_t(waves + 0.5));
+        g = (nblk == size_t(ap_ctx::kMaxBlocks)) ? ngroups : std::min(ngroups, g + wk * wave_groups);
+        waves *= AP_STREAM_GROWTH;
+      }
+    } else {
+      const size_t nb = std::min<size_t>({std::max<size_t>(ntasks / std::max<size_t>(total_warps / 2, 1), 1),
+                                          std::max<size_t>(ngroups, 1), 16});
+      const size_t gpb = (ngroups + nb - 1) / nb;
+      for (size_t g = 0; g < ngroups; g += gpb) blk_g0[nblk++] = g;
+    }
+    blk_g0[nblk] = ngroups;
+    if (!d2h_bound) {
+      CK(cudaEventRecord(c->ev_join, st));                    // code streams ready
+      CK(cudaStreamWaitEvent(c->stream_b, c->ev_join, 0));
+    }
     for (size_t k = 0; k < nblk; ++k) {
-      const size_t r0 = std::min(nrows, k * gpb * 2 * G), r1 = std::min(nrows, (k + 1) * gpb * 2 * G);
-      if (r0 >= r1) break;
-      cudaStream_t sk = (k & 1) ? c->stream_b : st;
+      const size_t r0 = std::min(nrows, blk_g0[k] * 2 * G), r1 = std::min(nrows, blk_g0[k + 1] * 2 * G);
+      cudaStream_t sk = (!d2h_bound && (k & 1)) ? c->stream_b : st;
       apk::CombParams pk = p;
       pk.xcode = c->d_xcode + r0 * h;
       pk.rows = uint32_t(r1 - r0);
       pk.row_global0 = uint32_t(row_global0 + r0);
       pk.out = p.out + (out_kind == 0 ? r0 * cols : 0);
       pk.out8 = p.out8 + (out_kind == 0 ? 0 : r0 * cols);
-      const size_t tk = ((r1 - r0 + 1) / 2 + G - 1) / G * nseg;
+      pk.S = uint32_t(Ss);
+      pk.nseg = uint32_t(nseg_s);
+      const size_t tk = ((r1 - r0 + 1) / 2 + G - 1) / G * nseg_s;
       const size_t gk = std::min<size_t>((tk + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta, size_t(c->sms) * per_sm);
       fn<<<dim3(unsigned(gk)), dim3(apk::kWarpsPerCta * 32), sh.smem, sk>>>(pk);
       CK(cudaGetLastError());
       CK(cudaEventRecord(c->ev_blk[k], sk));
       c->last_launches += 1;
-      ++launched;
-    }
-    CK(cudaEventRecord(c->ev_aux[1], c->stream_b));          // join the second stream
-    CK(cudaStreamWaitEvent(st, c->ev_aux[1], 0));
-    CK(cudaEventRecord(c->ev1, st));
-    for (size_t k = 0; k < launched; ++k) {
-      const size_t r0 = std::min(nrows, k * gpb * 2 * G), r1 = std::min(nrows, (k + 1) * gpb * 2 * G);
       CK(cudaStreamWaitEvent(c->stream_copy, c->ev_blk[k], 0));
       CK(cudaMemcpyAsync(static_cast<char*>(host_out) + r0 * cols * elem,
                          static_cast<const char*>(d_out) + r0 * cols * elem, (r1 - r0) * cols * elem,
                          cudaMemcpyDeviceToHost, c->stream_copy));
+    }
+    if (!d2h_bound) {
+      CK(cudaEventRecord(c->ev_join, c->stream_b));           // join the second stream
+      CK(cudaStreamWaitEvent(st, c->ev_join, 0));
+    }
+    CK(cudaEventRecord(c->ev1, st));
+    if (std::getenv("AP_TRACE")) {
+      for (size_t k = 0; k < nblk; ++k) CK(cudaEventRecord(c->ev_cp[k], c->stream_copy));
+      CK(cudaStreamSynchronize(c->stream_copy));
+      for (size_t k = 0; k < nblk; ++k) {
+        float tb = 0.f;
+        cudaEventElapsedTime(&tb, c->ev0, c->ev_blk[k]);
+        std::fprintf(stderr, "[ap trace] block %zu groups [%zu,%zu) comb done %.3f ms\n", k, blk_g0[k], blk_g0[k + 1], tb);
+      }
+      float tc = 0.f;
+      cudaEventElapsedTime(&tc, c->ev0, c->ev_cp[nblk - 1]);
+      std::fprintf(stderr, "[ap trace] copies done %.3f ms (nseg %zu, S %zu)\n", tc, nseg_s, Ss);
     }
     CK(cudaStreamSynchronize(c->stream_copy));
     return AP_OK;
@@ -640,8 +681,9 @@ int ap_ctx_create(int device, ap_ctx** out) {
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->stream_b, cudaStreamNonBlocking));
-  for (auto& e : c->ev_blk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  for (auto& e : c->ev_aux) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : c->ev_blk) CK(cudaEventCreate(&e));
+  for (auto& e : c->ev_cp) CK(cudaEventCreate(&e));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
   CK(cudaMalloc(&c->d_small, 64));
@@ -670,11 +712,12 @@ int ap_ctx_destroy(ap_ctx* c) {
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_cursor) cudaFreeHost(c->h_cursor);
   cudaStreamSynchronize(c->stream_copy);
+  cudaStreamSynchronize(c->stream_b);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
   for (auto& e : c->ev_blk) cudaEventDestroy(e);
-  for (auto& e : c->ev_aux) cudaEventDestroy(e);
-  cudaStreamSynchronize(c->stream_b);
+  for (auto& e : c->ev_cp) cudaEventDestroy(e);
+  cudaEventDestroy(c->ev_join);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->stream_copy);
   cudaStreamDestroy(c->stream_b);

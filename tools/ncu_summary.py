@@ -38,6 +38,18 @@ def main():
                  ("issue", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                  ("LSU shared wavefronts", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")]
         print("  pipes (% of peak):", ", ".join(f"{n} {float(d[k]):.1f}" for n, k in pipes if d.get(k)))
+        def num(k):
+            try:
+                return float(d[k].replace(",", ""))
+            except (KeyError, ValueError):
+                return None
+        rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+        units = dict(zip(rr[0], rr[1]))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        if rd is not None and wr is not None:
+            rb = rd * scale.get(units.get("dram__bytes_read.sum", "byte"), 1)
+            wb = wr * scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
+            print(f"  dram bytes per launch: read {rb:.0f} + write {wb:.0f} = {rb + wb:.0f}")
         pre = "smsp__pcsamp_warps_issue_stalled_"
         st = {k[len(pre):]: float(v.replace(",", "")) for k, v in d.items()
               if k.startswith(pre) and not k.endswith("_not_issued") and v.replace(",", "").replace(".", "").isdigit()}

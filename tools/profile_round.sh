@@ -21,5 +21,9 @@ for cr in C1:0 C2:0 C3:8192 C4:4096 C5:512; do
   python tools/prof_step.py --config $c --rows $n --reps 1 > $O/prof_$c.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:comb -c 1 -o $O/prof_$c \
         python tools/prof_step.py --config $c --rows $n --reps 1 > $O/ncu_full_$c.log 2>&1
+  # summarise on the box (gpurun brings back <= 64 MiB); keep only the C2 report
+  python tools/ncu_summary.py $O/prof_$c.ncu-rep --top 12 > $O/ncu_summary_$c.txt 2>&1
+  [ $c = C2 ] || rm -f $O/prof_$c.ncu-rep
 done
+python tools/d2h_bw.py > $O/d2h_bw.txt 2>&1
 ls -la $O
