@@ -395,3 +395,40 @@ def test_host_api_concurrent_threads():
     assert not errs, errs
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,u8", [("C2", False), ("C2", True)])
+def test_streamed_host_plot_equals_device_plot(name, u8):
+    """The host API streams the dense plot out in row blocks (D2H-bound uint16: short-task blocks
+    of growing size on one stream; compute-bound uint8: equal blocks on two streams); at C2's full
+    size (16285 x 16280, ~10 blocks) it must equal the one-launch device-API plot bit for bit,
+    and the rows at the block seams must equal the oracle."""
+    import ctypes
+
+    import torch
+
+    from paper_0909_2000_b200 import _native
+
+    c = datagen.CONFIGS[name]
+    x, y = datagen.make_inputs(name)
+    pc = cfg(c.w, c.h, c.r)
+    host = (ap.plot_dense_u8(x, y, pc) if u8 else ap.plot_dense_u16(x, y, pc)).reshape(-1)
+    L = _native.lib()
+    ctx = ctypes.c_void_p()
+    assert L.ap_ctx_create(0, ctypes.byref(ctx)) == 0
+    try:
+        dx, dy = torch.from_numpy(x.copy()).cuda(), torch.from_numpy(y.copy()).cuda()
+        dout = torch.empty(host.size, dtype=torch.uint8 if u8 else torch.int16, device="cuda")
+        fn = L.ap_ctx_plot_dense_u8_device if u8 else L.ap_ctx_plot_dense_device
+        assert fn(ctx, dx.data_ptr(), x.size, dy.data_ptr(), y.size, ctypes.byref(ap._cfg(pc)),
+                  dout.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        dev = dout.cpu().numpy().view(np.uint8 if u8 else np.uint16)
+    finally:
+        L.ap_ctx_destroy(ctx)
+    assert np.array_equal(host, dev)
+    rows, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
+    grid = host.reshape(rows, cols)
+    for rb in (887, 888, 2663, 2664):   # around the first block seams (148 pair groups of 6 rows)
+        rc, want = ol.plot_rows(x, y, c.w, c.h, c.r, rb, rb + 1)
+        assert rc == 0 and np.array_equal(grid[rb:rb + 1].astype(np.int32), want), rb
