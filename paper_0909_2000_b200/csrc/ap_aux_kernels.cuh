@@ -36,22 +36,70 @@ __global__ void xcode_kernel(const uint8_t* __restrict__ x, size_t m, const uint
 }
 
 // Alphabet of y: presence bitmap -> dense codes (map[b] = rank of b among the
-// bytes present in y, 0xFF if absent), sigma -> out[256].  One CTA.
+// bytes present in y, 0xFF if absent), sigma -> out[0], "byte 0 present" -> out[1].
+// One CTA of 1024 threads; the ranks come from a ballot prefix over 8 warps.
 __global__ void alphabet_kernel(const uint8_t* __restrict__ y, size_t n, uint8_t* __restrict__ map,
                                 uint32_t* __restrict__ sigma_out, uint32_t* __restrict__ zero_flag) {
   __shared__ uint32_t present[256];
+  __shared__ uint32_t wsum[8];
   for (int b = threadIdx.x; b < 256; b += blockDim.x) present[b] = 0;
   __syncthreads();
   for (size_t i = threadIdx.x; i < n; i += blockDim.x) present[y[i]] = 1;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t k = 0;
-    for (int b = 0; b < 256; ++b) {
-      map[b] = present[b] ? uint8_t(k) : uint8_t(0xFF);
-      k += present[b];
+  const uint32_t b = threadIdx.x, lane = b & 31u, wid = b >> 5;
+  const uint32_t pr = b < 256 ? present[b] : 0u;
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pr);
+  if (b < 256 && lane == 0) wsum[wid] = __popc(bal);
+  __syncthreads();
+  if (b < 256) {
+    uint32_t base = 0;
+    for (uint32_t k = 0; k < wid; ++k) base += wsum[k];
+    map[b] = pr ? uint8_t(base + __popc(bal & ((1u << lane) - 1u))) : uint8_t(0xFF);
+    if (b == 255) *sigma_out = base + __popc(bal);
+    if (b == 0) *zero_flag = pr;
+  }
+}
+
+// Fused code streams for small inputs (one launch instead of alphabet + xcode + ycode:
+// C1-sized plots are launch-bound): one CTA builds the alphabet map in shared memory
+// (as alphabet_kernel), writes sigma / the zero flag, clears the speculation abort flag,
+// then maps x and y like xcode_kernel and ycode_kernel.
+__global__ void codes_small_kernel(const uint8_t* __restrict__ x, size_t m, const uint8_t* __restrict__ y,
+                                   size_t n, uint32_t r, uint32_t sent, uint8_t* __restrict__ map,
+                                   uint32_t* __restrict__ small, uint8_t* __restrict__ xcode,
+                                   uint8_t* __restrict__ ycode, size_t total, uint32_t* __restrict__ ycol) {
+  __shared__ uint32_t present[256];
+  __shared__ uint32_t wsum[8];
+  __shared__ uint8_t smap[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) present[b] = 0;
+  __syncthreads();
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) present[y[i]] = 1;
+  __syncthreads();
+  const uint32_t b = threadIdx.x, lane = b & 31u, wid = b >> 5;
+  const uint32_t pr = b < 256 ? present[b] : 0u;
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pr);
+  if (b < 256 && lane == 0) wsum[wid] = __popc(bal);
+  __syncthreads();
+  if (b < 256) {
+    uint32_t base = 0;
+    for (uint32_t k = 0; k < wid; ++k) base += wsum[k];
+    const uint8_t code = pr ? uint8_t(base + __popc(bal & ((1u << lane) - 1u))) : uint8_t(0xFF);
+    smap[b] = code;
+    map[b] = code;
+    if (b == 255) small[0] = base + __popc(bal);
+    if (b == 0) { small[1] = pr; small[2] = 0u; }
+  }
+  __syncthreads();
+  for (size_t i = threadIdx.x; i < m; i += blockDim.x) xcode[i] = smap[x[i]];
+  const size_t N = n * r;
+  for (size_t c = threadIdx.x; c < total; c += blockDim.x) {
+    uint8_t v = 0;
+    if (c < N) v = (r == 2) ? ((c & 1) ? smap[y[c >> 1]] : uint8_t(sent)) : smap[y[c]];
+    ycode[c] = v;
+    if (ycol) {
+      ycol[c] = uint32_t(v) * 0x00010001u;
+      ycol[total + c] = 0u;
     }
-    *sigma_out = k;
-    *zero_flag = present[0];
   }
 }
 

@@ -77,6 +77,12 @@ struct CombParams {
   unsigned long long* cursor;     // staging append cursor
   unsigned long long stage_cap;
   uint32_t* seg_counts;           // [rows][nseg] hits per (row, segment)
+  // speculative alphabet (ap_capi.cu run_device): the launch was planned for an alphabet of
+  // at most sigma_cap codes before y's alphabet size reached the host; every warp checks the
+  // device-side size and, if it is larger, flags the launch for a re-run and exits
+  const uint32_t* sigma_dev;      // y's alphabet size (written by alphabet_kernel)
+  uint32_t sigma_cap;             // 0xFFFFFFFF: not speculative
+  uint32_t* abort_flag;
   uint32_t zero;                  // always 0 (HFMA2 addend)
   uint32_t one;                   // always 1 (IMAD forms the compiler must not fold)
   uint32_t minus_one;             // always 0xFFFFFFFF
@@ -594,6 +600,10 @@ comb_kernel(const CombParams p) {
   const uint32_t ngroups = (npairs + G - 1) / G;
   const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
   const uint64_t wstride = uint64_t(gridDim.x) * kWarpsPerCta;
+  if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
+    if (threadIdx.x == 0) *p.abort_flag = 1u;
+    return;
+  }
 
   for (uint64_t task = uint64_t(blockIdx.x) * kWarpsPerCta + warp; task < ntasks; task += wstride) {
     const uint32_t pg = uint32_t(task / p.nseg);
@@ -846,6 +856,10 @@ comb2_kernel(const CombParams p) {
   const uint32_t ngroups = (npairs + G - 1) / G;
   const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
   const uint64_t wstride = uint64_t(gridDim.x) * kWarpsPerCta;
+  if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
+    if (threadIdx.x == 0) *p.abort_flag = 1u;
+    return;
+  }
 
   for (uint64_t task = uint64_t(blockIdx.x) * kWarpsPerCta + warp; task < ntasks; task += wstride) {
     const uint32_t pg = uint32_t(task / p.nseg);

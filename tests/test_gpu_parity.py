@@ -432,3 +432,24 @@ def test_streamed_host_plot_equals_device_plot(name, u8):
     for rb in (887, 888, 2663, 2664):   # around the first block seams (148 pair groups of 6 rows)
         rc, want = ol.plot_rows(x, y, c.w, c.h, c.r, rb, rb + 1)
         assert rc == 0 and np.array_equal(grid[rb:rb + 1].astype(np.int32), want), rb
+
+
+def test_speculative_alphabet_plan_reruns_when_y_grows():
+    """Repeated calls plan for the previous call's alphabet size without waiting for this y's
+    (ap_capi.cu run_device): a call whose y has more codes must be detected on the device and
+    re-run; one with fewer codes runs on the larger plan.  Alternate alphabets of 2, 20, 4, 60
+    and 3 letters for the same (w, r, output) and check every dense and thresholded result."""
+    rng = np.random.default_rng(4242)
+    for r in (1, 2):
+        for sigma in (2, 20, 4, 60, 3, 60):
+            w = 24
+            x = rng.integers(1, sigma + 1, 300).astype(np.uint8)
+            y = np.concatenate([x[40:140], rng.integers(1, sigma + 1, 250)]).astype(np.uint8)
+            rc, want = ol.plot_rows(x, y, w, 1, r)
+            assert rc == 0
+            assert np.array_equal(gpu_grid(x, y, w, 1, r), want), (r, sigma)
+            assert np.array_equal(ap.plot_dense_u8(x, y, cfg(w, 1, r)).astype(np.int32), want), (r, sigma)
+            t = int(np.quantile(want, 0.97))
+            rr, cc = np.nonzero(want >= t)
+            gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
+            assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (r, sigma)
