@@ -173,6 +173,9 @@ constexpr int kSubUnroll = AP_SUBUNROLL;
 constexpr uint32_t kHfBase = 0x6400u;
 constexpr uint32_t kHfRebaseAt = 0x6400u + 0x3C0u;   // fresh keys stay < 0x6400 + 1024
 constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: rebase step >= 128 columns
+#ifndef AP_R2_SUBLOAD
+#define AP_R2_SUBLOAD 1   // r = 2 kernel, rolled sub loop: each sub prefetches its code words (no per-sub selects)
+#endif
 #ifndef AP_R2_ROWMAJOR
 #define AP_R2_ROWMAJOR 0   // 1: r = 2 step row pair by row pair (fewer $-row swap moves; B200: C2 +0.6%, C4 +0.7%)
 #endif
@@ -832,6 +835,7 @@ comb2_kernel(const CombParams p) {
   constexpr int NB = 2 * kChunk;   // blown bottom columns per chunk
   constexpr int kSubUnroll2 = RR <= AP_SUBUNROLL2_RR ? kChunk / 8 : 1;
   constexpr bool kFmaMin = RR >= AP_FMAMIN_RR;  // one of the two mismatch mins moves to the FMA pipe
+  constexpr bool kSubLoad = AP_R2_SUBLOAD && kSubUnroll2 == 1;   // C2 -0.5%; unrolled shapes: +3.7% (C4)
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
@@ -929,18 +933,40 @@ comb2_kernel(const CombParams p) {
     const uint32_t rebase_by = HF ? (kHfRebaseAt - kHfBase - 2 * kChunk - 2 * VB - p.W) & ~1u : kRebaseBy;
     uint32_t run = 0u, hitsA = 0u, hitsB = 0u;
 
-    uint4 ych = __ldg(reinterpret_cast<const uint4*>(yw));
-    uint4 ych2 = __ldg(reinterpret_cast<const uint4*>(yw) + 1);
-    if (j == 0) cd[0] = ych.x & 0xFFu;
+    // y codes: the unrolled sub loop (small RR) selects its words statically from two uint4
+    // per chunk; the rolled one (kSubLoad) reads code words 2s, 2s+1 and 2s+2 (the next
+    // step's code) per sub s, prefetched one sub ahead, instead of selecting by sub index
+    uint32_t w0n = 0, w1n = 0, w2n = 0, wi = 3;
+    uint4 ych = make_uint4(0, 0, 0, 0), ych2 = ych;
+    if constexpr (kSubLoad) {
+      w0n = __ldg(yw); w1n = __ldg(yw + 1); w2n = __ldg(yw + 2);
+      if (j == 0) cd[0] = w0n & 0xFFu;
+    } else {
+      ych = __ldg(reinterpret_cast<const uint4*>(yw));
+      ych2 = __ldg(reinterpret_cast<const uint4*>(yw) + 1);
+      if (j == 0) cd[0] = ych.x & 0xFFu;
+    }
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
-      const uint4 nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
-      const uint4 nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
+      uint4 nxa = make_uint4(0, 0, 0, 0), nxb = nxa;
+      if constexpr (!kSubLoad) {
+        nxa = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 2);
+        nxb = __ldg(reinterpret_cast<const uint4*>(yw) + 2 * ch + 3);
+      }
 #pragma unroll kSubUnroll2
       for (int sub = 0; sub < kChunk / 8; ++sub) {
-        const uint32_t w0 = sub == 0 ? ych.x : sub == 1 ? ych.z : sub == 2 ? ych2.x : ych2.z;
-        const uint32_t w1 = sub == 0 ? ych.y : sub == 1 ? ych.w : sub == 2 ? ych2.y : ych2.w;
-        const uint32_t w2 = sub == 0 ? ych.z : sub == 1 ? ych2.x : sub == 2 ? ych2.z : nxa.x;
+        uint32_t w0, w1, w2;
+        if constexpr (kSubLoad) {
+          w0 = w0n; w1 = w1n; w2 = w2n;
+          w0n = w2n;
+          w1n = __ldg(yw + wi);
+          w2n = __ldg(yw + wi + 1);
+          wi += 2;
+        } else {
+          w0 = sub == 0 ? ych.x : sub == 1 ? ych.z : sub == 2 ? ych2.x : ych2.z;
+          w1 = sub == 0 ? ych.y : sub == 1 ? ych.w : sub == 2 ? ych2.y : ych2.w;
+          w2 = sub == 0 ? ych.z : sub == 1 ? ych2.x : sub == 2 ? ych2.z : nxa.x;
+        }
         uint32_t* ring_sub = ringB + sub * 16;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
