@@ -123,16 +123,21 @@ int ap_ctx_create(int device, ap_ctx** out);
 int ap_ctx_destroy(ap_ctx* ctx);
 
 /* As ap_plot_dense, but x/y/out are device pointers on ctx's device and the
- * call only enqueues work on ctx's stream (stream 0 = the context's own).
- * Sentinel bytes are not checked (the host API checks them). */
+ * work runs on the given stream (0 = the context's own); the output is
+ * complete when the call returns.  The launch plan depends on y's alphabet
+ * size: the first call with a given (w, r, output) learns it with a stream
+ * synchronisation before the comb kernel; later calls plan for the previous
+ * size without waiting and have the kernel verify it on the device (the plot
+ * re-runs if y has more codes).  Sentinel bytes are not checked (the host API
+ * checks them). */
 int ap_ctx_plot_dense_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y,
                              size_t n, const ap_config* cfg, uint16_t* d_out, void* stream);
 
-/* As ap_plot_dense_u8 on device pointers (enqueue only). */
+/* As ap_plot_dense_u8 on device pointers (stream semantics of ap_ctx_plot_dense_device). */
 int ap_ctx_plot_dense_u8_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
                                 const ap_config* cfg, uint8_t* d_out, void* stream);
 
-/* As ap_plot_pgm on device pointers (enqueue only). */
+/* As ap_plot_pgm on device pointers (stream semantics of ap_ctx_plot_dense_device). */
 int ap_ctx_plot_pgm_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
                            const ap_config* cfg, uint8_t* d_pixels, void* stream);
 

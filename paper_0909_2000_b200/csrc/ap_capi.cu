@@ -683,9 +683,9 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     c->last_launches += 2;  // the two cub scan passes
     *nrec_out = nrec;
     *total_out = total;
-  } else if (speculate) {
-    // the dense device call completes before returning when its plan was speculative
-    CK(cudaMemcpyAsync(c->h_small, c->d_small, 12, cudaMemcpyDeviceToHost, st));
+  } else {
+    // a dense device call completes before returning (a speculative plan is verified here)
+    if (speculate) CK(cudaMemcpyAsync(c->h_small, c->d_small, 12, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
