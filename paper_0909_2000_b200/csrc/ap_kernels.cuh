@@ -48,6 +48,9 @@ namespace apk {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kChunk = 32;          // steps per extraction batch
+#ifndef AP_R2_STS64
+#define AP_R2_STS64 1   // r = 2 kernel: one 8-byte ring store per step (even ring stride; C2, C4 -1.1%)
+#endif
 constexpr uint32_t kRebaseAt = 0x7000u;   // fresh keys must stay fp16-finite (<= 0x7BFF)
 constexpr uint32_t kRebaseBy = 0x4000u;
 
@@ -108,7 +111,12 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 // only accumulate from lanes of the same group (j >= off).
 __host__ __device__ constexpr int groups_per_warp(int L) { return 32 / L; }
 __host__ __device__ constexpr int groups_alloc(int L) { return 32 / L + (32 % L ? 1 : 0); }
-__host__ __device__ constexpr int ring_stride(int L, int nb) { return L * ((nb + L - 1) / L) + 1; }
+// bottom-key ring words per group: nb entries rounded up to whole lanes, plus padding so
+// the bottom lanes of different groups write different banks; the r = 2 kernel (nb = 64)
+// keeps it even so a step's (2c, 2c+1) pair is one 8-byte store
+__host__ __device__ constexpr int ring_stride(int L, int nb) {
+  return L * ((nb + L - 1) / L) + (nb == 2 * kChunk && AP_R2_STS64 ? 2 - (L * ((nb + L - 1) / L)) % 2 : 1);
+}
 // ok-flag bytes per group: one u32 per ring slot (byte 0 = strip A, byte 2 =
 // strip B, so a slot reads back as the packed pair oA | oB << 16) plus 32 bytes
 // of padding so the same slot of different groups falls 8 banks apart.
@@ -1059,8 +1067,12 @@ comb2_kernel(const CombParams p) {
           }
 #endif
           if (j == lanes_real - 1) {
-            ring_sub[2 * u] = tbD[K - 1];
-            ring_sub[2 * u + 1] = tbR[K - 1];
+            if constexpr (AP_R2_STS64) {
+              *reinterpret_cast<uint2*>(ring_sub + 2 * u) = make_uint2(tbD[K - 1], tbR[K - 1]);
+            } else {
+              ring_sub[2 * u] = tbD[K - 1];
+              ring_sub[2 * u + 1] = tbR[K - 1];
+            }
           }
           {
             const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
