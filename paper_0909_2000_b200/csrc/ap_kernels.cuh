@@ -48,6 +48,9 @@ namespace apk {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kChunk = 32;          // steps per extraction batch
+#ifndef AP_G_STS64
+#define AP_G_STS64 1   // generic kernel: the bottom keys of two steps in one 8-byte ring store
+#endif
 #ifndef AP_R2_STS64
 #define AP_R2_STS64 1   // r = 2 kernel: one 8-byte ring store per step (even ring stride; C2, C4 -1.1%)
 #endif
@@ -115,7 +118,8 @@ __host__ __device__ constexpr int groups_alloc(int L) { return 32 / L + (32 % L 
 // the bottom lanes of different groups write different banks; the r = 2 kernel (nb = 64)
 // keeps it even so a step's (2c, 2c+1) pair is one 8-byte store
 __host__ __device__ constexpr int ring_stride(int L, int nb) {
-  return L * ((nb + L - 1) / L) + (nb == 2 * kChunk && AP_R2_STS64 ? 2 - (L * ((nb + L - 1) / L)) % 2 : 1);
+  return L * ((nb + L - 1) / L) + ((nb == 2 * kChunk && AP_R2_STS64) || (nb == kChunk && AP_G_STS64)
+                                      ? 2 - (L * ((nb + L - 1) / L)) % 2 : 1);
 }
 // ok-flag bytes per group: one u32 per ring slot (byte 0 = strip A, byte 2 =
 // strip B, so a slot reads back as the packed pair oA | oB << 16) plus 32 bytes
@@ -580,6 +584,9 @@ template <int L, int R, int K, bool DENSE, bool XM, bool HF>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
   constexpr int kHfRows = HF ? 1 : 0;   // rows of each quad whose V' is formed on the FMA pipe
+  // the bottom keys of two steps per 8-byte ring store (long lanes only: the 128-register
+  // shapes would spill the held key)
+  constexpr bool kSts64 = AP_G_STS64 && R > 16;
   static_assert(32 % L == 0 && L >= 4, "lane groups must tile the warp");
   constexpr int kSU = L < 8 ? 1 : kSubUnroll;   // L = 4 (R = 32): the bigger body runs best rolled
   static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
@@ -602,9 +609,10 @@ comb_kernel(const CombParams p) {
   // 64 B, so consecutive groups are shifted by 64 B to use the other bank half
   const size_t tgs = size_t(p.sigma) * Q * L + (L < 8 && p.sigma ? 4 : 0);
   const size_t tbytes = size_t(G) * tgs * 16;
-  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbytes) + g * (kChunk + 1);
+  constexpr int RSG = ring_stride(L, kChunk);
+  uint32_t* ringB = reinterpret_cast<uint32_t*>(wbase + tbytes) + g * RSG;
   const uint32_t okb = uint32_t(__cvta_generic_to_shared(wbase + tbytes)) +
-                       ((G * (kChunk + 1) * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
+                       ((G * RSG * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
   const uint32_t rshift = p.r - 1;
 
   const uint32_t npairs = (p.rows + 1) / 2;
@@ -685,6 +693,7 @@ comb_kernel(const CombParams p) {
 #pragma unroll
     for (int rho = 0; rho < R; ++rho) V[rho] = 0u;     // left-boundary seaweeds: key 0
     uint32_t tb[K];     // seaweed leaving band b at the previous step
+    uint32_t tb_prev = 0u;   // bottom key of the previous (even) step, stored with the next one
     uint32_t cd[K];     // y column word of band b at the current step
 #pragma unroll
     for (int b = 0; b < K; ++b) { tb[b] = 0u; cd[b] = 0u; }
@@ -753,7 +762,15 @@ comb_kernel(const CombParams p) {
             }
             tb[b] = t;
           }
-          if (j == L - 1) ring_sub[u] = tb[K - 1];
+          if constexpr (kSts64) {
+            if (u & 1) {
+              if (j == L - 1) *reinterpret_cast<uint2*>(ring_sub + u - 1) = make_uint2(tb_prev, tb[K - 1]);
+            } else {
+              tb_prev = tb[K - 1];
+            }
+          } else {
+            if (j == L - 1) ring_sub[u] = tb[K - 1];
+          }
           // codes of the next step: band b takes band b-1's, band 0 lane j-1's last band's
           {
             const uint32_t ynew = u == 0 ? qa.y : u == 1 ? qa.z : u == 2 ? qa.w : u == 3 ? qb.x :
