@@ -350,7 +350,7 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
 // out_kind (dense only): 0 = uint16 half-units into d_out, 1 = uint8 PGM pixels
 // (io.cpp:136-153 fused; cfg->has_threshold renders cells below it black).
 #ifndef AP_STREAM_GROWTH
-#define AP_STREAM_GROWTH 1.3
+#define AP_STREAM_GROWTH 1.2
 #endif
 
 int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
@@ -552,17 +552,22 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     // exposed ends.  The comb costs ~0.057 ps per blown cell, the D2H (PCIe, ~57 GB/s)
     // ~17.5 ps per byte on B200:
     //  * D2H-bound (uint16 output, W*r < ~600; C2): e2e = (time to the first finished
-    //    block) + D2H + ~50 us per copy.  Short tasks (segments of ~max(2048, 8W) columns:
-    //    ~0.4 ms per task on C2 instead of ~1.3 ms) on one stream, in row blocks of
-    //    round(1.3^k) full waves (equal tasks, so a block ends without a ragged tail; a
-    //    block's comb fits in the previous block's D2H, so the copy engine never idles):
-    //    the first copy starts after one task time, with ~8 copies in all.
+    //    block) + D2H + ~50 us per copy.  Short tasks (segments of ~max(1024, 4W) columns:
+    //    ~0.2 ms per task on C2 instead of ~1.3 ms; the extra W-1 overlap fits in the D2H
+    //    time) on one stream, in row blocks of round(1.2^k) full waves (equal tasks, so a
+    //    block ends without a ragged tail; a block's comb fits in the previous block's D2H,
+    //    so the copy engine never idles): the first copy starts after one task time.
+    //    (Swept on B200, AP_STREAM_S / AP_STREAM_GROWTH: 1024 / 1.2 best, 10.37 ms; 2048 /
+    //    1.3 10.57; 4096 / 1.45 10.63; two-stream equal blocks 11.07.)
     //  * compute-bound (1-byte output): normal segments, ~16 equal row blocks of at least
     //    half a wave alternating over two compute streams (consecutive blocks overlap), so
     //    only the last block's copy is exposed.
     const size_t elem = out_kind == 0 ? 2 : 1;
     const bool d2h_bound = double(elem) * 17.5 > 0.057 * double(W) * double(r);
-    size_t Ss = d2h_bound ? std::max<size_t>(2048, 8 * size_t(W)) : S;
+    size_t Ss = d2h_bound ? std::max<size_t>(1024, 4 * size_t(W)) : S;
+    if (const char* e = std::getenv("AP_STREAM_S")) Ss = std::max<size_t>(2 * W, std::strtoull(e, nullptr, 10));   // tuning
+    double growth = AP_STREAM_GROWTH;
+    if (const char* e = std::getenv("AP_STREAM_GROWTH")) growth = std::max(1.0, std::atof(e));   // tuning
     Ss = std::min(Ss, S);
     Ss = std::max<size_t>((Ss + salign - 1) / salign * salign, salign);
     const size_t nseg_s = (out_cols_eff + Ss - 1) / Ss;
@@ -576,7 +581,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
         blk_g0[nblk++] = g;
         const size_t wk = std::max<size_t>(1, size_t(waves + 0.5));
         g = (nblk == size_t(ap_ctx::kMaxBlocks)) ? ngroups : std::min(ngroups, g + wk * wave_groups);
-        waves *= AP_STREAM_GROWTH;
+        waves *= growth;
       }
     } else {
       const size_t nb = std::min<size_t>({std::max<size_t>(ntasks / std::max<size_t>(total_warps / 2, 1), 1),
