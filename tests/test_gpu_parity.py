@@ -429,7 +429,9 @@ def test_streamed_host_plot_equals_device_plot(name, u8):
     assert np.array_equal(host, dev)
     rows, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
     grid = host.reshape(rows, cols)
-    for rb in (887, 888, 2663, 2664):   # around the first block seams (148 pair groups of 6 rows)
+    # around the first block seams (one wave = 74 pair groups of 6 rows with 32 segments) and
+    # the old 148-group ones
+    for rb in (443, 444, 887, 888, 2663, 2664):
         rc, want = ol.plot_rows(x, y, c.w, c.h, c.r, rb, rb + 1)
         assert rc == 0 and np.array_equal(grid[rb:rb + 1].astype(np.int32), want), rb
 
