@@ -295,17 +295,18 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
 //  * Slot addresses and the running count use IMAD / IMAD.HI on the FMA pipe.
 // Packed 32-bit sums are exact whenever every half of the final value is in
 // [0, 0xFFFF] (arithmetic is linear mod 2^32), so no per-column bias is needed.
-template <int L, int NB, bool DENSE, bool CHECK>
-__device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t* ringB, uint32_t okb,
-                                              uint32_t rmask, uint32_t j, uint32_t g, uint32_t lane,
-                                              int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
-                                              uint32_t rA, uint32_t rB, bool hasA, bool hasB,
-                                              uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
+// Extraction phases (extract_body below chains them for one strip pair per group;
+// the two-pair r = 2 kernel, ap_kernels2p.cuh, runs the scatter and output phases once
+// per pair around one shared flag read and clear).  Shared constants:
+// phase 1: scatter the ok flags of countable seaweeds (bytes BYTE and BYTE + 2 of a slot:
+// strip A and B of the pair); cab[c]: bit 15 / 31 = column countable (strip A / B)
+template <int L, int NB, bool CHECK, int BYTE>
+__device__ __forceinline__ void extract_scatter(const CombParams& p, const uint32_t* ringB, uint32_t okb,
+                                                uint32_t rmask, uint32_t j, int32_t E0, uint32_t nseg_cols,
+                                                int32_t kbase, uint32_t* cab) {
   constexpr int CPL = (NB + L - 1) / L;   // columns per lane (the last lane may get fewer real ones)
   constexpr bool ALIGN = 32 % L == 0 && NB % L == 0;   // CPL is a power of two dividing 32
-  const uint32_t rshift = p.r - 1;
-  const uint32_t one = p.one;
-  const uint32_t k17 = one << 17, k18 = one << 18, k16 = one << 16;   // opaque: IMAD.HI, not LEA.HI
+  const uint32_t k18 = p.one << 18;   // opaque: IMAD.HI, not LEA.HI
   const int32_t W = int32_t(p.W);
   const int32_t eb = E0 + int32_t(j) * CPL;
   // delta aligns the read runs (eb - W + delta) and clear runs (E0 + A + delta + j*CPL) to CPL
@@ -316,9 +317,6 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
   const uint32_t n0 = (uint32_t(kbase + W - 1 - eb) & 0xFFFFu) * 0x00010001u;          // -(thr+1) at eb
   const uint32_t sb2 = (uint32_t(eb - W + 1 + int32_t(delta)) & rmask) * 0x00010001u;   // slot of start eb-W+1
   const uint32_t xA = okb * 0x00010001u + 0x20000u;   // addrA = imad(addrB, -65536, imad(slot2, 4, xA))
-
-  // ---- phase 1: scatter the ok flags of countable seaweeds
-  uint32_t cab[CPL];   // bit 15 / 31: column countable (strip A / B)
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int32_t e = eb + c;
@@ -334,13 +332,20 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
     cab[c] = ~pre & 0x80008000u;
     const uint32_t addrB = madhi(slot2, k18, okb + 2);          // okb + 4 * slotB + 2
     const uint32_t addrA = imad(addrB, 0xFFFF0000u, imad(slot2, 4u, xA));   // okb + 4 * slotA
-    sts_u8(addrA, 1u);
-    sts_u8(addrB, 1u);
+    sts_u8(addrA + BYTE, 1u);
+    sts_u8(addrB + BYTE, 1u);
   }
-  __syncwarp();
+}
 
-  // ---- phase 2: flags of starts e - W; acc = running sum of count deltas (countable - ok)
-  uint32_t o[CPL];
+// phase 2: the flag words of starts e - W (both pairs' bytes)
+template <int L, int NB, bool CHECK>
+__device__ __forceinline__ void extract_flags(const CombParams& p, uint32_t okb, uint32_t rmask, uint32_t j,
+                                              int32_t E0, uint32_t nseg_cols, uint32_t* o) {
+  constexpr int CPL = (NB + L - 1) / L;
+  constexpr bool ALIGN = 32 % L == 0 && NB % L == 0;
+  const int32_t W = int32_t(p.W);
+  const int32_t eb = E0 + int32_t(j) * CPL;
+  const uint32_t delta = ALIGN ? uint32_t(W - E0) & 31u : 0u;
   if constexpr (ALIGN) {
     const uint32_t rb = okb + 4 * (uint32_t(eb - W + int32_t(delta)) & rmask);
     if constexpr (CPL >= 4) {
@@ -367,13 +372,17 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
       if (valid) o[c] = lds_u32(okb + 4 * ((rsb + c) & rmask));
     }
   }
-  uint32_t acc = 0;
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    acc = imad(o[c], 0xFFFFFFFFu, madhi(cab[c], k17, acc));   // acc + countable - ok
-    cab[c] = acc;                                            // count delta through column c
-  }
-  // clear ahead: starts [E0 + A, E0 + A + NB), this lane's run of CPL
+}
+
+// clear ahead: starts [E0 + A, E0 + A + NB), this lane's run of CPL
+template <int L, int NB>
+__device__ __forceinline__ void extract_clear(const CombParams& p, uint32_t okb, uint32_t rmask, uint32_t j,
+                                              int32_t E0) {
+  constexpr int CPL = (NB + L - 1) / L;
+  constexpr bool ALIGN = 32 % L == 0 && NB % L == 0;
+  const int32_t W = int32_t(p.W);
+  const uint32_t delta = ALIGN ? uint32_t(W - E0) & 31u : 0u;
+  const uint32_t A = NB + (ALIGN ? uint32_t(-W) & uint32_t(CPL - 1) : 0u);
   {
     if constexpr (ALIGN) {
       const uint32_t cb = okb + 4 * (uint32_t(E0 + int32_t(A + delta) + int32_t(j) * CPL) & rmask);
@@ -391,6 +400,27 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
       for (int c = 0; c < CPL; ++c)
         if (NB % L == 0 || j * CPL + c < NB) sts_u32(okb + 4 * ((cb + c) & rmask), 0u);
     }
+  }
+}
+
+// phase 3: count deltas (cab = countable bits, o = this pair's flag halves) -> group
+// scan -> dense half-units or threshold hits for rows rA, rB
+template <int L, int NB, bool DENSE, bool CHECK>
+__device__ __forceinline__ void extract_out(const CombParams& p, uint32_t j, uint32_t g, uint32_t lane,
+                                            int32_t E0, uint32_t nseg_cols, uint32_t c0, uint32_t* cab,
+                                            const uint32_t* o, uint32_t rA, uint32_t rB, bool hasA, bool hasB,
+                                            uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
+  constexpr int CPL = (NB + L - 1) / L;
+  const uint32_t rshift = p.r - 1;
+  const uint32_t one = p.one;
+  const uint32_t k17 = one << 17, k16 = one << 16;   // opaque: IMAD.HI, not LEA.HI
+  const int32_t W = int32_t(p.W);
+  const int32_t eb = E0 + int32_t(j) * CPL;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    acc = imad(o[c], 0xFFFFFFFFu, madhi(cab[c], k17, acc));   // acc + countable - ok
+    cab[c] = acc;                                            // count delta through column c
   }
   // group scan of the lane totals; count after column c = run + excl + acc_c
   uint32_t incl = acc;
@@ -538,6 +568,22 @@ __device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t
       hitsB += gtot >> 16;
     }
   }
+}
+
+template <int L, int NB, bool DENSE, bool CHECK>
+__device__ __forceinline__ void extract_body(const CombParams& p, const uint32_t* ringB, uint32_t okb,
+                                              uint32_t rmask, uint32_t j, uint32_t g, uint32_t lane,
+                                              int32_t E0, uint32_t nseg_cols, int32_t kbase, uint32_t c0,
+                                              uint32_t rA, uint32_t rB, bool hasA, bool hasB,
+                                              uint32_t& run, uint32_t& hitsA, uint32_t& hitsB) {
+  constexpr int CPL = (NB + L - 1) / L;
+  uint32_t cab[CPL], o[CPL];
+  extract_scatter<L, NB, CHECK, 0>(p, ringB, okb, rmask, j, E0, nseg_cols, kbase, cab);
+  __syncwarp();
+  extract_flags<L, NB, CHECK>(p, okb, rmask, j, E0, nseg_cols, o);
+  extract_clear<L, NB>(p, okb, rmask, j, E0);
+  extract_out<L, NB, DENSE, CHECK>(p, j, g, lane, E0, nseg_cols, c0, cab, o, rA, rB, hasA, hasB, run, hitsA,
+                                   hitsB);
 }
 
 // Chunks whose bottom columns and window starts all lie inside the segment
