@@ -188,9 +188,6 @@ constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: reba
 #ifndef AP_R2_SUBLOAD
 #define AP_R2_SUBLOAD 1   // r = 2 kernel, rolled sub loop: each sub prefetches its code words (no per-sub selects)
 #endif
-#ifndef AP_R2_ROWMAJOR
-#define AP_R2_ROWMAJOR 0   // 1: r = 2 step row pair by row pair (fewer $-row swap moves; B200: C2 +0.6%, C4 +0.7%)
-#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -1057,37 +1054,6 @@ comb2_kernel(const CombParams p) {
             for (int b = 1; b < K; ++b) { tinD[b] = tbD[b - 1]; tinR[b] = tbR[b - 1]; }
           }
           fresh += 0x00020002u;
-#if AP_R2_ROWMAJOR
-          // Row pair by row pair, both blown columns at once.  $ row 2i: the
-          // ($,$) swap sends the old V down column 2c and takes column 2c's
-          // seaweed, which then meets column 2c+1's (never a match): down =
-          // max, V = min.  Real row 2i+1: ($ col) max/min, then (real, real).
-          // The old $-row V is consumed before its new value is written, so
-          // every V keeps its register across steps (no swap moves).
-#pragma unroll
-          for (int b = 0; b < K; ++b) {
-            uint32_t tD = tinD[b], tR = tinR[b];
-#pragma unroll
-            for (int i = 0; i < RRB; ++i) {
-              uint32_t& vs = V[b * 2 * RRB + 2 * i];
-              uint32_t& vr = V[b * 2 * RRB + 2 * i + 1];
-              const uint32_t dD = vs;                          // down column 2c
-              const uint32_t dR = __vmaxu2(tD, tR);            // down column 2c+1
-              uint32_t nvs;
-              if constexpr (kFmaMin) nvs = imad(dR, p.minus_one, imad(tD, p.one, tR));   // min = tD + tR - max
-              else nvs = __vminu2(tD, tR);
-              const uint32_t eD = __vmaxu2(vr, dD);
-              const uint32_t vr1 = __vminu2(vr, dD);
-              const uint32_t eR = __viaddmax_s16x2(dR, m[b][i], vr1);
-              vr = lop3_xor(vr1, dR, eR);
-              vs = nvs;
-              tD = eD;
-              tR = eR;
-            }
-            tbD[b] = tD;
-            tbR[b] = tR;
-          }
-#else
 #pragma unroll
           for (int b = 0; b < K; ++b) {
             uint32_t t = tinD[b];                       // blown column 2c: $
@@ -1128,7 +1094,6 @@ comb2_kernel(const CombParams p) {
             }
             tbR[b] = t;
           }
-#endif
           if (j == lanes_real - 1) {
             if constexpr (AP_R2_STS64) {
               *reinterpret_cast<uint2*>(ring_sub + 2 * u) = make_uint2(tbD[K - 1], tbR[K - 1]);
