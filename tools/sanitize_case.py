@@ -21,3 +21,15 @@ xb = rng.integers(1, 61, 300).astype(np.uint8)   # large alphabet -> computed-ma
 yb = rng.integers(1, 61, 400).astype(np.uint8)
 ap.plot_dense_u16(xb, yb, ap.PlotConfig(window_w=121, step_h=5, blowup_r=2, mode=ap.Mode.cuda))
 print("sanitize case ok")
+# repeated calls: the speculative alphabet plan + fused code-stream kernel, and a plan re-run
+for s in (4, 4, 20, 4):
+    xs = rng.integers(1, s + 1, 500).astype(np.uint8)
+    ys = rng.integers(1, s + 1, 600).astype(np.uint8)
+    ap.plot_dense_u16(xs, ys, ap.PlotConfig(window_w=48, step_h=1, blowup_r=2, mode=ap.Mode.cuda))
+    ap.plot_dense_u8(xs, ys, ap.PlotConfig(window_w=48, step_h=1, blowup_r=1, mode=ap.Mode.cuda))
+# fp16-key kernels across several rebases, and a streamed host plot of several row blocks
+xl = rng.integers(1, 5, 2600).astype(np.uint8)
+yl = rng.integers(1, 5, 3000).astype(np.uint8)
+ap.plot_dense_u16(xl, yl, ap.PlotConfig(window_w=100, step_h=1, blowup_r=2, mode=ap.Mode.cuda))
+ap.plot_dense_u16(xl, yl, ap.PlotConfig(window_w=128, step_h=1, blowup_r=1, mode=ap.Mode.cuda))
+print("sanitize case (extended) ok")
