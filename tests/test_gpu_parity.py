@@ -455,3 +455,31 @@ def test_speculative_alphabet_plan_reruns_when_y_grows():
             rr, cc = np.nonzero(want >= t)
             gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
             assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (r, sigma)
+
+
+def test_tiny_windows_and_degenerate_alphabets():
+    """w = 1..8 in both modes and steps 1..3, a one-letter y, x letters absent from y, and y of
+    exactly w characters (one column) -- the smallest shapes of every code path."""
+    rng = np.random.default_rng(99)
+    cases = []
+    for w in range(1, 9):
+        for r in (1, 2):
+            for h in (1, 3):
+                x = rng.integers(1, 5, w + 40).astype(np.uint8)
+                y = rng.integers(1, 5, w + 70).astype(np.uint8)
+                cases.append((x, y, w, h, r))
+    one = np.full(90, 7, np.uint8)
+    cases.append((rng.integers(6, 9, 60).astype(np.uint8), one, 12, 1, 1))   # one-letter y
+    cases.append((rng.integers(6, 9, 60).astype(np.uint8), one, 12, 2, 2))
+    cases.append((rng.integers(20, 24, 80).astype(np.uint8), rng.integers(1, 5, 120).astype(np.uint8), 16, 1, 1))
+    xw = rng.integers(1, 5, 50).astype(np.uint8)
+    cases.append((xw, xw[5:35].copy(), 30, 1, 1))                             # y of exactly w characters
+    cases.append((xw, xw[5:35].copy(), 30, 1, 2))
+    for x, y, w, h, r in cases:
+        rc, want = ol.plot_rows(x, y, w, h, r)
+        assert rc == 0
+        assert np.array_equal(gpu_grid(x, y, w, h, r), want), (w, h, r, x.size, y.size)
+        t = int(want.max())
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (w, h, r)
