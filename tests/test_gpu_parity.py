@@ -483,3 +483,43 @@ def test_tiny_windows_and_degenerate_alphabets():
         rr, cc = np.nonzero(want >= t)
         gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
         assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (w, h, r)
+
+
+def test_threshold_staging_overflow_rerun():
+    """More hits than the staging area (65536 records on a fresh context) and than the caller's
+    capacity: the kernel re-runs with exact staging, the call reports AP_CAPACITY with the exact
+    count, and a second call with that capacity returns the oracle's row-major list."""
+    import ctypes
+
+    import torch
+
+    from paper_0909_2000_b200 import _native
+
+    rng = np.random.default_rng(5)
+    x = rng.integers(1, 5, 420).astype(np.uint8)
+    y = rng.integers(1, 5, 400).astype(np.uint8)
+    w, h, r, t = 20, 1, 1, 0            # every cell is a hit: 401 x 381 = 152781 > 65536
+    rc, want = ol.plot_rows(x, y, w, h, r)
+    er, ec = np.nonzero(want >= t)
+    L = _native.lib()
+    ctx = ctypes.c_void_p()
+    assert L.ap_ctx_create(0, ctypes.byref(ctx)) == 0
+    try:
+        dx, dy = torch.from_numpy(x.copy()).cuda(), torch.from_numpy(y.copy()).cuda()
+        c = ap._cfg(cfg(w, h, r, t))
+        count = ctypes.c_uint64()
+        small = 1000
+        dr, dc, dh = (torch.empty(small, dtype=dt, device="cuda") for dt in (torch.int32, torch.int32, torch.int16))
+        rc = L.ap_ctx_plot_threshold_device(ctx, dx.data_ptr(), x.size, dy.data_ptr(), y.size, ctypes.byref(c),
+                                            ctypes.byref(count), dr.data_ptr(), dc.data_ptr(), dh.data_ptr(), small,
+                                            None)
+        assert rc == _native.AP_CAPACITY and count.value == er.size
+        n = count.value
+        dr, dc, dh = (torch.empty(n, dtype=dt, device="cuda") for dt in (torch.int32, torch.int32, torch.int16))
+        rc = L.ap_ctx_plot_threshold_device(ctx, dx.data_ptr(), x.size, dy.data_ptr(), y.size, ctypes.byref(c),
+                                            ctypes.byref(count), dr.data_ptr(), dc.data_ptr(), dh.data_ptr(), n, None)
+        assert rc == 0 and count.value == n
+        assert np.array_equal(dr.cpu().numpy(), er) and np.array_equal(dc.cpu().numpy(), ec)
+        assert np.array_equal(dh.cpu().numpy().astype(np.int32), want[er, ec])
+    finally:
+        L.ap_ctx_destroy(ctx)
