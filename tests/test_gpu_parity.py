@@ -523,3 +523,18 @@ def test_threshold_staging_overflow_rerun():
         assert np.array_equal(dh.cpu().numpy().astype(np.int32), want[er, ec])
     finally:
         L.ap_ctx_destroy(ctx)
+
+
+@pytest.mark.parametrize("w,r,sigma", [(128, 1, 4), (100, 2, 4), (64, 2, 20)])
+def test_plot_transpose_symmetry_mid_size(w, r, sigma):
+    """Size-independent property at a size the oracle cannot check whole: the window LCS and the
+    alignment score are symmetric, so plot(x, y) == plot(y, x)^T (different kernels' row/column
+    roles, segments and extraction chunks), here on ~6000 x 5000 grids."""
+    rng = np.random.default_rng(w * 10 + r)
+    x = rng.integers(1, sigma + 1, 6000).astype(np.uint8)
+    y = np.concatenate([x[1000:3500], rng.integers(1, sigma + 1, 2600)]).astype(np.uint8)
+    a = ap.plot_dense_u16(x, y, cfg(w, 1, r))
+    b = ap.plot_dense_u16(y, x, cfg(w, 1, r))
+    assert np.array_equal(a, b.T)
+    rc, want = ol.plot_rows(x, y, w, 1, r, 2500, 2502)   # plus two rows against the oracle
+    assert rc == 0 and np.array_equal(a[2500:2502].astype(np.int32), want)
