@@ -538,3 +538,54 @@ def test_plot_transpose_symmetry_mid_size(w, r, sigma):
     assert np.array_equal(a, b.T)
     rc, want = ol.plot_rows(x, y, w, 1, r, 2500, 2502)   # plus two rows against the oracle
     assert rc == 0 and np.array_equal(a[2500:2502].astype(np.int32), want)
+
+
+def test_c2_full_grid_transpose_symmetry():
+    """C2 at full size (16285 x 16280 alignment-score plot): plot(x, y) == plot(y, x)^T."""
+    c = datagen.CONFIGS["C2"]
+    x, y = datagen.make_inputs("C2")
+    a = ap.plot_dense_u16(x, y, cfg(c.w, c.h, c.r))
+    b = ap.plot_dense_u16(y, x, cfg(c.w, c.h, c.r))
+    assert a.shape == (x.size - c.w + 1, y.size - c.w + 1) and np.array_equal(a, b.T)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_threshold_list_transpose_symmetry(name):
+    """C3 / C4 at full size: the thresholded list of (x, y) is the transposed list of (y, x)
+    (C4: 2.17e6 hits of a 262081 x 262081 plot, row-major order on both sides)."""
+    c = datagen.CONFIGS[name]
+    x, y = datagen.make_inputs(name)
+    r1, c1, h1 = ap.plot_threshold_arrays(x, y, cfg(c.w, c.h, c.r), c.t_half)
+    r2, c2, h2 = ap.plot_threshold_arrays(y, x, cfg(c.w, c.h, c.r), c.t_half)
+    assert r1.size == r2.size
+    # transpose (y, x)'s list and put it in row-major order
+    o = np.lexsort((r2, c2))
+    assert np.array_equal(r1, c2[o]) and np.array_equal(c1, r2[o]) and np.array_equal(h1, h2[o])
+    assert np.all(np.diff(r1.astype(np.int64) * (1 << 32) + c1) > 0)   # strictly row-major
+
+
+def _mix64(v):
+    """splitmix64 finaliser on uint64 arrays (order-independent list checksums)."""
+    v = (v ^ (v >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    v = (v ^ (v >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return v ^ (v >> np.uint64(31))
+
+
+def test_c5_full_size_threshold_checksum_symmetry():
+    """C5 at full size (1048321 x 1048321 LCS plot, 1.03e8 hits at WLCS >= 180): the list of
+    (x, y) and the transposed list of (y, x) have the same count and the same order-independent
+    checksum of (row, col, half); each list is strictly row-major."""
+    c = datagen.CONFIGS["C5"]
+    x, y = datagen.make_inputs("C5")
+    sums = []
+    for a, b, swap in ((x, y, False), (y, x, True)):
+        rr, cc, hh = ap.plot_threshold_arrays(a, b, cfg(c.w, c.h, c.r), c.t_half)
+        key = rr.astype(np.uint64) * np.uint64(1 << 32) + cc.astype(np.uint64)
+        assert np.all(np.diff(key.astype(np.int64)) > 0)
+        if swap:
+            rr, cc = cc, rr
+        k = (rr.astype(np.uint64) << np.uint64(32)) | cc.astype(np.uint64)
+        with np.errstate(over="ignore"):
+            sums.append((rr.size, int(np.sum(_mix64(k ^ (hh.astype(np.uint64) << np.uint64(50))), dtype=np.uint64))))
+        del rr, cc, hh, key, k
+    assert sums[0] == sums[1]
