@@ -4,7 +4,7 @@
 CFGS=$1; shift
 for v in "$@"; do
   if [ "$v" = base ]; then unset AP_LIB_PATH; else export AP_LIB_PATH=tools/exp/$v/libalignplot_b200.so; fi
-  r=$(python -m pytest tests/test_gpu_parity.py -x -q -k "reference_grids or random or acceptance or threshold" 2>&1 | tail -1)
+  r=$(python -m pytest tests/test_gpu_parity.py -x -q -k "(reference_grids or random or acceptance or threshold) and not full_size and not c5_full" 2>&1 | tail -1)
   echo "$v parity: $r"
   for cr in $CFGS; do
     c=${cr%%:*}; n=${cr##*:}
