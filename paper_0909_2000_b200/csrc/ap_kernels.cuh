@@ -185,6 +185,9 @@ constexpr int kSubUnroll = AP_SUBUNROLL;
 constexpr uint32_t kHfBase = 0x6400u;
 constexpr uint32_t kHfRebaseAt = 0x6400u + 0x3C0u;   // fresh keys stay < 0x6400 + 1024
 constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: rebase step >= 128 columns
+#ifndef AP_HF_ROWS
+#define AP_HF_ROWS 1   // generic fp16-key kernels: rows of each quad whose V' is formed by two HADD2s
+#endif
 #ifndef AP_R2_SUBLOAD
 #define AP_R2_SUBLOAD 1   // r = 2 kernel, rolled sub loop: each sub prefetches its code words (no per-sub selects)
 #endif
@@ -626,7 +629,7 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 template <int L, int R, int K, bool DENSE, bool XM, bool HF>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
 comb_kernel(const CombParams p) {
-  constexpr int kHfRows = HF ? 1 : 0;   // rows of each quad whose V' is formed on the FMA pipe
+  constexpr int kHfRows = HF ? AP_HF_ROWS : 0;   // rows of each quad whose V' is formed on the FMA pipe
   // the bottom keys of two steps per 8-byte ring store (long lanes only: the 128-register
   // shapes would spill the held key)
   constexpr bool kSts64 = AP_G_STS64 && R > 16;
