@@ -226,6 +226,7 @@ bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
 // Launch plan for (W, w, r, sigma, dense): kernel shape, function, occupancy.
 struct LaunchPlan {
   Shape sh;
+  int wpc = apk::kWarpsPerCta;   // warps per CTA of the launches
   bool spec = false;
   apk::KernelFn fn = nullptr;
   int per_sm = 0;
@@ -425,10 +426,12 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf)
                         : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm, plan.sh.hf);
     if (!plan.fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", plan.sh.L, plan.sh.R);
+    // warps per CTA, as compiled into the kernel (ap_kernels.cuh kGenericWpc / r2_wpc)
+    plan.wpc = plan.spec ? apk::r2_wpc(plan.sh.R / 2) : apk::kGenericWpc;
+    plan.sh.smem = plan.sh.smem / apk::kWarpsPerCta * plan.wpc;   // shapes are sized for 4-warp CTAs
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.sh.smem)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&plan.per_sm, plan.fn, apk::kWarpsPerCta * 32,
-                                                     plan.sh.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&plan.per_sm, plan.fn, plan.wpc * 32, plan.sh.smem));
     if (plan.per_sm < 1) return fail(AP_CONFIG, "kernel L=%d R=%d does not fit an SM", plan.sh.L, plan.sh.R);
     if (!overrides) c->plans[pkey] = plan;
   }
@@ -469,7 +472,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   KernelFn fn = plan.fn;
   const int per_sm = plan.per_sm;
-  const size_t total_warps = size_t(c->sms) * per_sm * apk::kWarpsPerCta;
+  const int wpc = plan.wpc;
+  const size_t total_warps = size_t(c->sms) * per_sm * wpc;
 
   // column segments: enough independent (strip pair, segment) tasks for ~4
   // waves, each segment at least 4 windows wide to bound the W-1 overlap.
@@ -522,7 +526,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.has_pgm_threshold = cfg->has_threshold ? 1u : 0u;
 
   const size_t ntasks = ngroups * nseg;
-  const size_t ctas_needed = (ntasks + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta;
+  const size_t ctas_needed = (ntasks + wpc - 1) / wpc;
   const size_t grid = std::min<size_t>(ctas_needed, size_t(c->sms) * per_sm);
 
   if (!dense) {
@@ -606,8 +610,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       pk.S = uint32_t(Ss);
       pk.nseg = uint32_t(nseg_s);
       const size_t tk = ((r1 - r0 + 1) / 2 + G - 1) / G * nseg_s;
-      const size_t gk = std::min<size_t>((tk + apk::kWarpsPerCta - 1) / apk::kWarpsPerCta, size_t(c->sms) * per_sm);
-      fn<<<dim3(unsigned(gk)), dim3(apk::kWarpsPerCta * 32), sh.smem, sk>>>(pk);
+      const size_t gk = std::min<size_t>((tk + wpc - 1) / wpc, size_t(c->sms) * per_sm);
+      fn<<<dim3(unsigned(gk)), dim3(wpc * 32), sh.smem, sk>>>(pk);
       CK(cudaGetLastError());
       CK(cudaEventRecord(c->ev_blk[k], sk));
       c->last_launches += 1;
@@ -641,7 +645,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
                         d_orow, d_ocol, d_ohalf, cap, out_kind, host_out, false);
     return AP_OK;
   }
-  fn<<<dim3(unsigned(grid)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(p);
+  fn<<<dim3(unsigned(grid)), dim3(wpc * 32), sh.smem, st>>>(p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev1, st));
   c->last_launches += 1;
@@ -672,7 +676,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       p.stage = c->d_stage;
       p.stage_cap = c->cap_stage;
       CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
-      fn<<<dim3(unsigned(grid)), dim3(apk::kWarpsPerCta * 32), sh.smem, st>>>(p);
+      fn<<<dim3(unsigned(grid)), dim3(wpc * 32), sh.smem, st>>>(p);
       CK(cudaGetLastError());
       c->last_launches += 1;
     }

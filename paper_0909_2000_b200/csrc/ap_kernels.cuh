@@ -46,7 +46,13 @@
 
 namespace apk {
 
-constexpr int kWarpsPerCta = 4;
+constexpr int kWarpsPerCta = 4;   // warps per CTA the shapes' shared memory and occupancy are sized for
+// Warps per CTA of the launches: one-warp CTAs release an SM's resources warp by warp as the
+// grid drains (B200: C4 -8.5%, C3 -2.5%, C5 -2% against 4-warp CTAs), except the r = 2 shapes
+// with long lanes (RR >= 8: C2 +3% with one-warp CTAs).  Compile-time, so a one-warp CTA's
+// shared-memory base is a constant; the host mirrors the rule (launch_wpc in ap_capi.cu).
+constexpr int kGenericWpc = 1;
+__host__ __device__ constexpr int r2_wpc(int rr) { return rr >= 8 ? 4 : 1; }
 constexpr int kChunk = 32;          // steps per extraction batch
 #ifndef AP_G_STS64
 #define AP_G_STS64 1   // generic kernel: the bottom keys of two steps in one 8-byte ring store
@@ -627,8 +633,9 @@ __device__ __forceinline__ void extract_chunk(const CombParams& p, const uint32_
 //   A = ~((xpair ^ y * 0x10001) + 0x7FFF7FFF) & 0x80008000 (bit 15 of a half
 //   survives iff the codes are equal).
 template <int L, int R, int K, bool DENSE, bool XM, bool HF>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, R <= 16 ? 4 : (R <= 24 ? 3 : 2))
+__global__ void __launch_bounds__(kGenericWpc * 32, (R <= 16 ? 4 : (R <= 24 ? 3 : 2)) * 4 / kGenericWpc)
 comb_kernel(const CombParams p) {
+  constexpr int WPC = kGenericWpc;
   constexpr int kHfRows = HF ? AP_HF_ROWS : 0;   // rows of each quad whose V' is formed on the FMA pipe
   // the bottom keys of two steps per 8-byte ring store (long lanes only: the 128-register
   // shapes would spill the held key)
@@ -645,7 +652,7 @@ comb_kernel(const CombParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
-  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t warp = WPC == 1 ? 0u : threadIdx.x >> 5;
   const uint32_t g = lane / L;
   const uint32_t j = lane % L;
   const size_t per_warp = comb_smem_per_warp(L, R, p.sigma, p.ring);
@@ -664,13 +671,13 @@ comb_kernel(const CombParams p) {
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + G - 1) / G;
   const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
-  const uint64_t wstride = uint64_t(gridDim.x) * kWarpsPerCta;
+  const uint64_t wstride = uint64_t(gridDim.x) * WPC;
   if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
     if (threadIdx.x == 0) *p.abort_flag = 1u;
     return;
   }
 
-  for (uint64_t task = uint64_t(blockIdx.x) * kWarpsPerCta + warp; task < ntasks; task += wstride) {
+  for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task += wstride) {
     const uint32_t pg = uint32_t(task / p.nseg);
     const uint32_t seg = uint32_t(task % p.nseg);
     const uint32_t pair = pg * G + g;
@@ -895,8 +902,9 @@ __device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t*
 }
 
 template <int L, int RR, int K, bool DENSE, bool HF>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, RR <= AP_R2_MB4 ? 4 : (RR <= 16 ? 3 : 2))
+__global__ void __launch_bounds__(r2_wpc(RR) * 32, (RR <= AP_R2_MB4 ? 4 : (RR <= 16 ? 3 : 2)) * 4 / r2_wpc(RR))
 comb2_kernel(const CombParams p) {
+  constexpr int WPC = r2_wpc(RR);
   static_assert(L <= 32 && RR % K == 0, "bad shape");
   constexpr int G = groups_per_warp(L);     // real groups; lanes >= G*L are idle
   constexpr int R = 2 * RR;
@@ -910,7 +918,7 @@ comb2_kernel(const CombParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
-  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t warp = WPC == 1 ? 0u : threadIdx.x >> 5;
   const uint32_t g = lane / L;
   const uint32_t j = lane % L;
   const size_t per_warp = comb_smem_per_warp(L, K * BW, p.sigma, p.ring, NB);
@@ -930,13 +938,13 @@ comb2_kernel(const CombParams p) {
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + G - 1) / G;
   const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
-  const uint64_t wstride = uint64_t(gridDim.x) * kWarpsPerCta;
+  const uint64_t wstride = uint64_t(gridDim.x) * WPC;
   if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
     if (threadIdx.x == 0) *p.abort_flag = 1u;
     return;
   }
 
-  for (uint64_t task = uint64_t(blockIdx.x) * kWarpsPerCta + warp; task < ntasks; task += wstride) {
+  for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task += wstride) {
     const uint32_t pg = uint32_t(task / p.nseg);
     const uint32_t seg = uint32_t(task % p.nseg);
     const uint32_t pair = pg * G + g;
