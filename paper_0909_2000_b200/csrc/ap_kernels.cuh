@@ -52,7 +52,10 @@ constexpr int kWarpsPerCta = 4;   // warps per CTA the shapes' shared memory and
 // with long lanes (RR >= 8: C2 +3% with one-warp CTAs).  Compile-time, so a one-warp CTA's
 // shared-memory base is a constant; the host mirrors the rule (launch_wpc in ap_capi.cu).
 constexpr int kGenericWpc = 1;
-__host__ __device__ constexpr int r2_wpc(int rr) { return rr >= 8 ? 4 : 1; }
+#ifndef AP_R2_LONG_WPC
+#define AP_R2_LONG_WPC 4
+#endif
+__host__ __device__ constexpr int r2_wpc(int rr) { return rr >= 8 ? AP_R2_LONG_WPC : 1; }
 constexpr int kChunk = 32;          // steps per extraction batch
 #ifndef AP_G_STS64
 #define AP_G_STS64 1   // generic kernel: the bottom keys of two steps in one 8-byte ring store
