@@ -257,6 +257,7 @@ struct ap_ctx {
   uint4* d_stage = nullptr;
   size_t cap_stage = 0;
   unsigned long long* d_cursor = nullptr;
+  uint32_t* d_tasks = nullptr;   // per-launch task counters (AP_DYN_TASKS)
   unsigned long long* h_cursor = nullptr;  // pinned
   uint32_t* d_segc = nullptr;
   size_t cap_segc = 0;
@@ -552,6 +553,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     p.seg_counts = c->d_segc;
   }
 
+  p.task_counter = c->d_tasks + 62;
+  if (AP_DYN_TASKS) CK(cudaMemsetAsync(c->d_tasks, 0, 64 * sizeof(uint32_t), st));
   CK(cudaEventRecord(c->ev0, st));
   if (dense && host_out) {
     // Dense output to the host: the plot streams out row block by row block while later
@@ -614,6 +617,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       pk.nseg = uint32_t(nseg_s);
       const size_t tk = ((r1 - r0 + 1) / 2 + G - 1) / G * nseg_s;
       const size_t gk = std::min<size_t>((tk + wpc - 1) / wpc, size_t(c->sms) * per_sm);
+      pk.task_counter = c->d_tasks + k;
       fn<<<dim3(unsigned(gk)), dim3(wpc * 32), sh.smem, sk>>>(pk);
       CK(cudaGetLastError());
       CK(cudaEventRecord(c->ev_blk[k], sk));
@@ -679,6 +683,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       p.stage = c->d_stage;
       p.stage_cap = c->cap_stage;
       CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
+      p.task_counter = c->d_tasks + 63;
       fn<<<dim3(unsigned(grid)), dim3(wpc * 32), sh.smem, st>>>(p);
       CK(cudaGetLastError());
       c->last_launches += 1;
@@ -756,6 +761,7 @@ int ap_ctx_create(int device, ap_ctx** out) {
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
   CK(cudaMalloc(&c->d_small, 64));
+  CK(cudaMalloc(&c->d_tasks, 64 * sizeof(uint32_t)));
   CK(cudaMallocHost(&c->h_small, 64));
   CK(cudaMalloc(&c->d_map, 256));
   CK(cudaMalloc(&c->d_cursor, 16));
@@ -774,7 +780,7 @@ int ap_ctx_destroy(ap_ctx* c) {
   DevGuard dg(c->device);
   cudaStreamSynchronize(c->stream);
   for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_ycol, (void*)c->d_map,
-                  (void*)c->d_small, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
+                  (void*)c->d_small, (void*)c->d_tasks, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
                   (void*)c->d_segc, (void*)c->d_offs, c->d_cub, (void*)c->d_orow, (void*)c->d_ocol,
                   (void*)c->d_ohalf})
     if (p) cudaFree(p);

@@ -90,6 +90,7 @@ struct CombParams {
   int32_t t_half;
   uint4* stage;                   // {row, col, half, rank} records
   unsigned long long* cursor;     // staging append cursor
+  uint32_t* task_counter;         // AP_DYN_TASKS: tasks handed out after the first static wave (zeroed per launch)
   unsigned long long stage_cap;
   uint32_t* seg_counts;           // [rows][nseg] hits per (row, segment)
   // speculative alphabet (ap_capi.cu run_device): the launch was planned for an alphabet of
@@ -104,6 +105,25 @@ struct CombParams {
 };
 
 using KernelFn = void (*)(CombParams);
+
+// Task distribution: every warp starts with task (CTA, warp); after that, warps claim the next
+// unclaimed task from a per-launch global counter, so warps that run faster (fewer co-resident
+// warps, fewer threshold hits, ...) take more tasks and the grid drains evenly (B200: C4 -7%,
+// C5 -2%, C2 and C3 -1% against a static stride).
+#ifndef AP_DYN_TASKS
+#define AP_DYN_TASKS 1
+#endif
+__device__ __forceinline__ uint64_t next_task(const CombParams& p, uint64_t task, uint64_t wstride, uint32_t lane,
+                                              uint64_t ntasks) {
+  if constexpr (AP_DYN_TASKS) {
+    if (ntasks <= wstride) return ntasks;   // one static wave covers the launch
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(p.task_counter, 1u);
+    return uint64_t(__shfl_sync(0xFFFFFFFFu, t, 0)) + wstride;
+  } else {
+    return task + wstride;
+  }
+}
 // Launch-stub pointers of the instantiated comb kernels (ap_inst_l{8,16,32}.cu).
 KernelFn pick_l4(int r, int k, bool dense, bool xm);
 KernelFn pick_l8(int r, int k, bool dense, bool xm);
@@ -680,7 +700,7 @@ comb_kernel(const CombParams p) {
     return;
   }
 
-  for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task += wstride) {
+  for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task = next_task(p, task, wstride, lane, ntasks)) {
     const uint32_t pg = uint32_t(task / p.nseg);
     const uint32_t seg = uint32_t(task % p.nseg);
     const uint32_t pair = pg * G + g;
@@ -947,7 +967,7 @@ comb2_kernel(const CombParams p) {
     return;
   }
 
-  for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task += wstride) {
+  for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task = next_task(p, task, wstride, lane, ntasks)) {
     const uint32_t pg = uint32_t(task / p.nseg);
     const uint32_t seg = uint32_t(task % p.nseg);
     const uint32_t pair = pg * G + g;
