@@ -520,6 +520,25 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.sent_code = sent;
   p.S = uint32_t(S);
   p.nseg = uint32_t(nseg);
+  p.g_split = uint32_t(ngroups);   // no short tail tasks unless set below
+  p.nseg2 = p.nseg;
+  p.S2 = p.S;
+  // Dense r = 2 plots: the last ~wave of work as tasks of half the segment width.  The dynamic
+  // task counter hands them out last, so the grid drains on short tasks instead of leaving
+  // SMs idle while the last full-length tasks finish (C2: 5.92 -> 5.56 ms; halves beat
+  // quarters, 5.61, and a two-wave tail, 5.58).  AP_TAIL_SPLIT=1 disables it (tuning).
+  size_t tail_div = 2;
+  if (const char* e = std::getenv("AP_TAIL_SPLIT")) tail_div = size_t(std::max(1, std::atoi(e)));
+  if (spec && dense && !host_out && nseg > 1 && tail_div > 1) {
+    size_t S2 = std::max<size_t>((S / tail_div + salign - 1) / salign * salign, std::max<size_t>(2 * W, salign));
+    const size_t nseg2 = (out_cols_eff + S2 - 1) / S2;
+    double tail_waves = 1.0;
+    if (const char* e = std::getenv("AP_TAIL_WAVES")) tail_waves = std::atof(e);
+    const size_t g2 = std::min(ngroups, std::max<size_t>(1, size_t(tail_waves * double(total_warps) / double(nseg2))));
+    p.g_split = uint32_t(ngroups - g2);
+    p.nseg2 = uint32_t(nseg2);
+    p.S2 = uint32_t(S2);
+  }
   p.ring = sh.ring;
   p.cols = uint32_t(cols);
   p.row_global0 = uint32_t(row_global0);
@@ -529,7 +548,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.pgm_threshold = cfg->threshold_half;
   p.has_pgm_threshold = cfg->has_threshold ? 1u : 0u;
 
-  const size_t ntasks = ngroups * nseg;
+  const size_t ntasks = size_t(p.g_split) * nseg + (ngroups - p.g_split) * p.nseg2;
   const size_t ctas_needed = (ntasks + wpc - 1) / wpc;
   const size_t grid = std::min<size_t>(ctas_needed, size_t(c->sms) * per_sm);
 

@@ -77,6 +77,9 @@ struct CombParams {
   uint32_t sent_code;     // code of the $ sentinel (r = 2)
   uint32_t S;             // column segment width (effective columns), multiple of 32
   uint32_t nseg;          // number of column segments
+  // dense r = 2 launches: pair groups >= g_split are cut into nseg2 segments of S2 columns
+  // (short tasks claimed last, so the grid drains on them); g_split = all groups: none
+  uint32_t g_split, nseg2, S2;
   uint32_t ring;          // ok-flag ring size (power of two >= W + 64)
   uint32_t cols;          // grid columns
   uint32_t row_global0;   // global grid row of local row 0
@@ -960,7 +963,9 @@ comb2_kernel(const CombParams p) {
   const uint32_t VB = lanes_real * K;           // virtual bands down to the strip bottom
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + G - 1) / G;
-  const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
+  const uint32_t gsplit = min(p.g_split, ngroups);
+  const uint64_t split_tasks = uint64_t(gsplit) * p.nseg;
+  const uint64_t ntasks = split_tasks + uint64_t(ngroups - gsplit) * p.nseg2;
   const uint64_t wstride = uint64_t(gridDim.x) * WPC;
   if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
     if (threadIdx.x == 0) *p.abort_flag = 1u;
@@ -968,14 +973,22 @@ comb2_kernel(const CombParams p) {
   }
 
   for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task = next_task(p, task, wstride, lane, ntasks)) {
-    const uint32_t pg = uint32_t(task / p.nseg);
-    const uint32_t seg = uint32_t(task % p.nseg);
+    CombParams pt = p;   // this task's segment width (short tail tasks: S2)
+    uint32_t pg, seg;
+    if (task < split_tasks) {
+      pg = uint32_t(task / p.nseg);
+      seg = uint32_t(task % p.nseg);
+    } else {
+      pg = gsplit + uint32_t((task - split_tasks) / p.nseg2);
+      seg = uint32_t((task - split_tasks) % p.nseg2);
+      pt.S = p.S2;
+    }
     const uint32_t pair = pg * G + g;
     const uint32_t rA = 2 * pair, rB = 2 * pair + 1;
     const bool hasA = g < uint32_t(G) && rA < p.rows, hasB = g < uint32_t(G) && rB < p.rows;
-    const uint32_t c0 = seg * p.S;                         // blown, multiple of 64
+    const uint32_t c0 = seg * pt.S;                        // blown, multiple of 64
     const uint32_t c0r = c0 >> 1;                          // raw, multiple of 32
-    const uint32_t nseg_cols = min(p.S + p.W - 1, p.N - c0);
+    const uint32_t nseg_cols = min(pt.S + p.W - 1, p.N - c0);
     const uint32_t nraw = (nseg_cols + 1) >> 1;
     const uint32_t nsteps = nraw + VB - 1;
     const uint32_t nch = (nsteps + kChunk - 1) / kChunk;
@@ -1149,7 +1162,7 @@ comb2_kernel(const CombParams p) {
       ych = nxa;
       ych2 = nxb;
       __syncwarp();
-      extract_chunk<L, NB, DENSE>(p, ringB, okb, okmask, j, g, lane,
+      extract_chunk<L, NB, DENSE>(pt, ringB, okb, okmask, j, g, lane,
                                   2 * (int32_t(ch * kChunk) - int32_t(VB - 1)), nseg_cols, kbase, c0, rA,
                                   rB, hasA, hasB, run, hitsA, hitsB);
       if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= (HF ? kHfRebaseAt : kRebaseAt)) {
