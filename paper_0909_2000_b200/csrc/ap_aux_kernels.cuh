@@ -104,17 +104,19 @@ __global__ void codes_small_kernel(const uint8_t* __restrict__ x, size_t m, cons
 }
 
 // Deterministic row-major placement of staged threshold records:
-// final index = offset[row * nseg + seg] + rank.
+// final index = offset[row * seg_stride + seg] + rank, where rows below split_row are cut into
+// segments of seg_cols columns and the rest (the launch's short tail tasks) of seg_cols2.
 __global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long nrec,
-                             const unsigned long long* __restrict__ offsets, uint32_t nseg,
-                             uint32_t seg_cols, uint32_t r, uint32_t row_global0,
-                             uint32_t* __restrict__ orow, uint32_t* __restrict__ ocol,
+                             const unsigned long long* __restrict__ offsets, uint32_t seg_stride,
+                             uint32_t seg_cols, uint32_t seg_cols2, uint32_t split_row, uint32_t r,
+                             uint32_t row_global0, uint32_t* __restrict__ orow, uint32_t* __restrict__ ocol,
                              uint16_t* __restrict__ ohalf, unsigned long long cap) {
   for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < nrec;
        i += 1ull * gridDim.x * blockDim.x) {
     const uint4 rec = stage[i];
-    const uint32_t seg = (rec.y * r) / seg_cols;
-    const unsigned long long pos = offsets[size_t(rec.x - row_global0) * nseg + seg] + rec.w;
+    const uint32_t row = rec.x - row_global0;
+    const uint32_t seg = (rec.y * r) / (row < split_row ? seg_cols : seg_cols2);
+    const unsigned long long pos = offsets[size_t(row) * seg_stride + seg] + rec.w;
     if (pos < cap) {
       orow[pos] = rec.x;
       ocol[pos] = rec.y;

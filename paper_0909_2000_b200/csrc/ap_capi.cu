@@ -523,13 +523,14 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.g_split = uint32_t(ngroups);   // no short tail tasks unless set below
   p.nseg2 = p.nseg;
   p.S2 = p.S;
-  // Dense r = 2 plots: the last ~wave of work as tasks of half the segment width.  The dynamic
-  // task counter hands them out last, so the grid drains on short tasks instead of leaving
-  // SMs idle while the last full-length tasks finish (C2: 5.92 -> 5.56 ms; halves beat
-  // quarters, 5.61, and a two-wave tail, 5.58).  AP_TAIL_SPLIT=1 disables it (tuning).
+  // The last ~wave of work as tasks of half the segment width.  The dynamic task counter
+  // hands them out last, so the grid drains on short tasks instead of leaving SMs idle while
+  // the last full-length tasks finish (C2: 5.92 -> 5.56 ms; halves beat quarters, 5.61, and
+  // a two-wave tail, 5.58).  Launches of at least two waves; the streamed dense host path has
+  // short tasks of its own.  AP_TAIL_SPLIT=1 disables it (tuning).
   size_t tail_div = 2;
   if (const char* e = std::getenv("AP_TAIL_SPLIT")) tail_div = size_t(std::max(1, std::atoi(e)));
-  if (spec && dense && !host_out && nseg > 1 && tail_div > 1) {
+  if (!(dense && host_out) && tail_div > 1 && ngroups * nseg >= 2 * total_warps && S / tail_div >= 2 * W) {
     size_t S2 = std::max<size_t>((S / tail_div + salign - 1) / salign * salign, std::max<size_t>(2 * W, salign));
     const size_t nseg2 = (out_cols_eff + S2 - 1) / S2;
     double tail_waves = 1.0;
@@ -539,6 +540,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     p.nseg2 = uint32_t(nseg2);
     p.S2 = uint32_t(S2);
   }
+  p.seg_stride = std::max(p.nseg, p.nseg2);
+  const size_t split_row = size_t(p.g_split) * 2 * G;   // first local row of the short-task groups
   p.ring = sh.ring;
   p.cols = uint32_t(cols);
   p.row_global0 = uint32_t(row_global0);
@@ -559,9 +562,12 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       if (rc2) return rc2;
     }
     // one extra zero slot so the exclusive scan also yields the total
-    if ((rc = grow(&c->d_segc, &c->cap_segc, nrows * nseg + 1))) return rc;
-    if ((rc = grow(&c->d_offs, &c->cap_offs, nrows * nseg + 1))) return rc;
-    CK(cudaMemsetAsync(c->d_segc + nrows * nseg, 0, sizeof(uint32_t), st));
+    const size_t nc = nrows * p.seg_stride;
+    if ((rc = grow(&c->d_segc, &c->cap_segc, nc + 1))) return rc;
+    if ((rc = grow(&c->d_offs, &c->cap_offs, nc + 1))) return rc;
+    // with a tail split the rows of the long-task groups leave counts nseg..seg_stride-1 unset
+    if (p.seg_stride != p.nseg) CK(cudaMemsetAsync(c->d_segc, 0, (nc + 1) * sizeof(uint32_t), st));
+    else CK(cudaMemsetAsync(c->d_segc + nc, 0, sizeof(uint32_t), st));
     CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
     // the kernel tests h >= t in biased 16-bit halves: |h| <= 2048, so clamping t
     // to +-0x4000 keeps every comparison exact
@@ -678,7 +684,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   if (!dense) {
     // deterministic row-major placement: exclusive scan of (row, segment) counts
-    const size_t nc = nrows * nseg;
+    const size_t nc = nrows * p.seg_stride;
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->d_segc, c->d_offs, int(nc + 1), st));
     if (c->cap_cub < tmp) {
@@ -709,8 +715,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     }
     if (nrec && d_orow) {
       const size_t blocks = std::min<size_t>((nrec + 255) / 256, 8192);
-      apk::place_kernel<<<unsigned(blocks), 256, 0, st>>>(c->d_stage, nrec, c->d_offs,
-                                                            uint32_t(nseg), uint32_t(S), r,
+      apk::place_kernel<<<unsigned(blocks), 256, 0, st>>>(c->d_stage, nrec, c->d_offs, p.seg_stride,
+                                                            uint32_t(S), p.S2, uint32_t(split_row), r,
                                                             uint32_t(row_global0), d_orow, d_ocol,
                                                             d_ohalf, cap);
       CK(cudaGetLastError());

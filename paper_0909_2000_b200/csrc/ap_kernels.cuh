@@ -77,9 +77,10 @@ struct CombParams {
   uint32_t sent_code;     // code of the $ sentinel (r = 2)
   uint32_t S;             // column segment width (effective columns), multiple of 32
   uint32_t nseg;          // number of column segments
-  // dense r = 2 launches: pair groups >= g_split are cut into nseg2 segments of S2 columns
-  // (short tasks claimed last, so the grid drains on them); g_split = all groups: none
+  // pair groups >= g_split are cut into nseg2 segments of S2 columns (short tasks claimed
+  // last, so the grid drains on them); g_split = all groups: none
   uint32_t g_split, nseg2, S2;
+  uint32_t seg_stride;    // row stride of seg_counts (max(nseg, nseg2))
   uint32_t ring;          // ok-flag ring size (power of two >= W + 64)
   uint32_t cols;          // grid columns
   uint32_t row_global0;   // global grid row of local row 0
@@ -95,7 +96,7 @@ struct CombParams {
   unsigned long long* cursor;     // staging append cursor
   uint32_t* task_counter;         // AP_DYN_TASKS: tasks handed out after the first static wave (zeroed per launch)
   unsigned long long stage_cap;
-  uint32_t* seg_counts;           // [rows][nseg] hits per (row, segment)
+  uint32_t* seg_counts;           // [rows][seg_stride] hits per (row, segment)
   // speculative alphabet (ap_capi.cu run_device): the launch was planned for an alphabet of
   // at most sigma_cap codes before y's alphabet size reached the host; every warp checks the
   // device-side size and, if it is larger, flags the launch for a re-run and exits
@@ -696,7 +697,9 @@ comb_kernel(const CombParams p) {
 
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + G - 1) / G;
-  const uint64_t ntasks = uint64_t(ngroups) * p.nseg;
+  const uint32_t gsplit = min(p.g_split, ngroups);
+  const uint64_t split_tasks = uint64_t(gsplit) * p.nseg;
+  const uint64_t ntasks = split_tasks + uint64_t(ngroups - gsplit) * p.nseg2;
   const uint64_t wstride = uint64_t(gridDim.x) * WPC;
   if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
     if (threadIdx.x == 0) *p.abort_flag = 1u;
@@ -704,13 +707,21 @@ comb_kernel(const CombParams p) {
   }
 
   for (uint64_t task = uint64_t(blockIdx.x) * WPC + warp; task < ntasks; task = next_task(p, task, wstride, lane, ntasks)) {
-    const uint32_t pg = uint32_t(task / p.nseg);
-    const uint32_t seg = uint32_t(task % p.nseg);
+    CombParams pt = p;   // this task's segment width (short tail tasks: S2)
+    uint32_t pg, seg;
+    if (task < split_tasks) {
+      pg = uint32_t(task / p.nseg);
+      seg = uint32_t(task % p.nseg);
+    } else {
+      pg = gsplit + uint32_t((task - split_tasks) / p.nseg2);
+      seg = uint32_t((task - split_tasks) % p.nseg2);
+      pt.S = p.S2;
+    }
     const uint32_t pair = pg * G + g;
     const uint32_t rA = 2 * pair, rB = 2 * pair + 1;
     const bool hasA = rA < p.rows, hasB = rB < p.rows;
-    const uint32_t c0 = seg * p.S;
-    const uint32_t nseg_cols = min(p.S + p.W - 1, p.N - c0);
+    const uint32_t c0 = seg * pt.S;
+    const uint32_t nseg_cols = min(pt.S + p.W - 1, p.N - c0);
     const uint32_t nsteps = nseg_cols + VB - 1;
     const uint32_t nch = (nsteps + kChunk - 1) / kChunk;
 
@@ -864,7 +875,7 @@ comb_kernel(const CombParams p) {
       }
       __syncwarp();
 
-      extract_chunk<L, kChunk, DENSE>(p, ringB, okb, p.ring - 1, j, g, lane,
+      extract_chunk<L, kChunk, DENSE>(pt, ringB, okb, p.ring - 1, j, g, lane,
                                       int32_t(ch * kChunk) - (VB - 1), nseg_cols, kbase, c0, rA, rB,
                                       hasA, hasB, run, hitsA, hitsB);
 
@@ -882,8 +893,8 @@ comb_kernel(const CombParams p) {
     }
     if constexpr (!DENSE) {
       if (j == 0) {
-        if (hasA) p.seg_counts[size_t(rA) * p.nseg + seg] = hitsA;
-        if (hasB) p.seg_counts[size_t(rB) * p.nseg + seg] = hitsB;
+        if (hasA) p.seg_counts[size_t(rA) * p.seg_stride + seg] = hitsA;
+        if (hasB) p.seg_counts[size_t(rB) * p.seg_stride + seg] = hitsB;
       }
     }
   }
@@ -1181,8 +1192,8 @@ comb2_kernel(const CombParams p) {
     }
     if constexpr (!DENSE) {
       if (j == 0) {
-        if (hasA) p.seg_counts[size_t(rA) * p.nseg + seg] = hitsA;
-        if (hasB) p.seg_counts[size_t(rB) * p.nseg + seg] = hitsB;
+        if (hasA) p.seg_counts[size_t(rA) * p.seg_stride + seg] = hitsA;
+        if (hasB) p.seg_counts[size_t(rB) * p.seg_stride + seg] = hitsB;
       }
     }
   }
