@@ -479,8 +479,6 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   // column segments: enough independent (strip pair, segment) tasks for ~4
   // waves, each segment at least 4 windows wide to bound the W-1 overlap.
   const int G = 32 / sh.L;
-  const size_t VB = size_t(sh.L) * sh.K;
-  (void)VB;
   const size_t npairs = (nrows + 1) / 2;
   const size_t ngroups = (npairs + G - 1) / G;
   const size_t out_cols_eff = (N - W) + 1;  // window starts in effective columns (stride 1)
