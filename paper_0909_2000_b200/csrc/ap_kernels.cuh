@@ -221,6 +221,9 @@ constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: reba
 #ifndef AP_HF_ROWS
 #define AP_HF_ROWS 1   // generic fp16-key kernels: rows of each quad whose V' is formed by two HADD2s
 #endif
+#ifndef AP_SUBUNROLL_L4
+#define AP_SUBUNROLL_L4 2   // generic kernel, L = 4 shapes: unroll of the 8-step sub loop (C3 -0.5% vs 1)
+#endif
 #ifndef AP_R2_SUBLOAD
 #define AP_R2_SUBLOAD 1   // r = 2 kernel, rolled sub loop: each sub prefetches its code words (no per-sub selects)
 #endif
@@ -668,7 +671,7 @@ comb_kernel(const CombParams p) {
   // shapes would spill the held key)
   constexpr bool kSts64 = AP_G_STS64 && R > 16;
   static_assert(32 % L == 0 && L >= 4, "lane groups must tile the warp");
-  constexpr int kSU = L < 8 ? 1 : kSubUnroll;   // L = 4 (R = 32): the bigger body runs best rolled
+  constexpr int kSU = L < 8 ? AP_SUBUNROLL_L4 : kSubUnroll;
   static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
   constexpr int G = 32 / L;
   constexpr int Q = R / 4;        // quads per lane
