@@ -24,17 +24,25 @@ def main():
     a = argparse.ArgumentParser()
     a.add_argument("--n", type=int, default=400)
     a.add_argument("--seed", type=int, default=1)
+    a.add_argument("--big", action="store_true", help="large windows (W up to 1024) and long y, few rows")
     args = a.parse_args()
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
     cells = 0
     for it in range(args.n):
         r = 1 + int(rng.integers(0, 2))
-        w = int(rng.integers(1, 300 if r == 1 else 150))
-        h = int(rng.choice([1, 1, 1, 2, 3, 5, 7]))
-        sigma = int(rng.choice([2, 4, 4, 20, 60, 200]))
-        m = int(rng.integers(w, w + 600))
-        n = int(rng.integers(w, w + 3000))
+        if args.big:
+            w = int(rng.integers(300, 1025 if r == 1 else 513))
+            h = int(rng.choice([1, 1, 2]))
+            sigma = int(rng.choice([4, 4, 20]))
+            m = int(rng.integers(w, w + 24))
+            n = int(rng.integers(w, w + 40000))
+        else:
+            w = int(rng.integers(1, 300 if r == 1 else 150))
+            h = int(rng.choice([1, 1, 1, 2, 3, 5, 7]))
+            sigma = int(rng.choice([2, 4, 4, 20, 60, 200]))
+            m = int(rng.integers(w, w + 600))
+            n = int(rng.integers(w, w + 3000))
         x = rng.integers(1, sigma + 1, m).astype(np.uint8)
         if rng.random() < 0.5:   # planted homology
             y = np.concatenate([rng.integers(1, sigma + 1, n // 3), x[: min(m, n // 2)],
