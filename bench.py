@@ -1,31 +1,35 @@
 #!/usr/bin/env python3
 """Benchmark of the alignment-plot hot path (BASELINE.json metric: window-pair cell updates/s).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl engine|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--scaling strong|weak]
+                  [--impl engine|reference]
 
 A *step* is one pass of the hot path over one full plot of the workload: the
 code-stream kernels plus the fused comb+extract kernel writing the dense
-uint16 grid (C1/C2) or the thresholded row-major list (C3-C5).  The default
-workload is BASELINE.json configs[1] = C2 (alignment-score plot, m=16384,
-w=100, dense), which fits one B200.
+uint16 grid (C1/C2) or the thresholded row-major list (C3-C5; scan + placement
+of every hit).  The default workload is BASELINE.json configs[3] = C4 (the
+config its "1/2/4/8 B200" metric is quoted on: alignment-score plot, sigma=20,
+m=n=262144, w=64, score >= 16), which fits one B200.
 
-* ``value``  — WPCU/s = rows*cols*w / t over all ranks, inputs resident in HBM
-  (ap_ctx_*_device), timed with CUDA events on the launching stream, L2
-  flushed (256 MiB write) between steps outside the timed events.
-* ``e2e``    — the same metric through the public host API (ap_plot_dense /
-  ap_plot_threshold) with pinned host buffers: H2D of x,y and D2H of the plot
-  inside the timed region.
-* ``roofline`` — the comb kernel against the measured integer-ALU issue peak
-  (profiles/int_peak_r01.json x the SM clock sampled during the run); the
-  algorithmic work is 3 int32 lane-ops per comb cell (SURVEY.md §8d basis),
-  comb cells = rows * (w*r) * (n*r).
-* ``cpu_baseline`` — the unmodified reference library (oracle/_ref, sea8 /
-  sea16, all host cores) on a bounded row sample of the same workload.
+* ``value``  -- WPCU/s = rows*cols*w / t of the whole plot, inputs resident in HBM
+  (ap_ctx_*_device), timed with CUDA events on the launching stream (max over
+  ranks), L2 flushed (256 MiB write) between steps outside the timed events.
+* ``e2e``    -- the same metric through the public host API (ap_plot_dense /
+  ap_plot_threshold) with pinned host buffers: H2D of x, y and D2H of the plot
+  or list inside the timed region.
+* ``roofline`` -- the comb kernel's ALU instructions (its minimal count per comb
+  cell, kernel_alu_ops_per_cell) per second against the measured ALU-pipe issue
+  peak (profiles/int_peak_r01.json x the SM clock sampled during the run), so
+  ``frac`` <= 1; ``vs_generic_recurrence`` keeps SURVEY.md §8d's basis (3 int32
+  lane-ops per comb cell).  Comb cells = rows * (w*r) * (n*r).
+* ``cpu_baseline`` -- the unmodified reference library (oracle/_ref, sea8 /
+  sea16, all host cores) on a bounded, evenly spaced row sample; ``parity``
+  compares the timed output with the reference on exactly those rows.
 
-Multi-GPU (torchrun): rows of an N-times-taller x (the workload's x followed by
-seeded uniform DNA) shard over ranks with a w-1 halo; per-rank work is fixed
-(weak scaling); the time is the max over ranks; thresholded configs all_gather
-one hit count per rank (NCCL), dense ones exchange nothing.
+Multi-GPU (torchrun): grid rows shard over ranks in contiguous blocks with a w-1
+x halo.  ``--scaling strong`` (C4, C5) splits the config's fixed plot;
+``--scaling weak`` (C1-C3) grows x with the rank count.  No data-path collective:
+thresholded configs all_gather one hit count per rank (NCCL).
 """
 from __future__ import annotations
 
@@ -125,38 +129,56 @@ class ClockSampler:
 
 
 # ---- workload -------------------------------------------------------------------------------
-def workload(name: str, world: int):
+def default_scaling(name: str) -> str:
+    """C4 / C5 are the fixed plots BASELINE.json shards over 1/2/4/8 GPUs (strong); the smaller
+    configs grow x with the rank count (weak)."""
+    return "strong" if name in ("C4", "C5") else "weak"
+
+
+def workload(name: str, world: int, scaling: str):
     c = datagen.CONFIGS[name]
     x, y = datagen.make_inputs(name)
-    if world > 1:
+    if world > 1 and scaling == "weak":
         # weak scaling: x grows by world; each rank gets the base workload's row count
         extra = datagen.uniform(1000 + world, 7, (world - 1) * x.size, datagen.DNA if name != "C4" else datagen.PROTEIN)
         x = np.concatenate([x, extra])
     return c, x, y
 
 
-def kernel_ceiling(kernel: str, peak_ops_clk: float):
-    """Comb cells per SM clock at which the chosen kernel saturates the ALU pipe (cells count
-    both strips of a packed u32).  Generic kernel per u32 = one cell of each of two strips:
-    VIADDMNMX + LOP3 (2 ALU ops); fp16 keys move one row in four's LOP3 to two HADD2s on the
-    FMA pipe (1.75); computed masks add LOP3 + IADD + LOP3 (5).  r = 2 kernel per u32 block of
-    2 x 2 blown cells x two strips: 3 VIMNMX + VIADDMNMX + LOP3 (5 ALU ops; the ($,$) swap is
-    free, the other mismatch min runs on the FMA pipe as two IMADs or two HADD2s)."""
+# ALU-pipe instructions per comb cell of each kernel family (both strips of a packed u32 counted
+# as two cells); the kernel's useful ALU work, the numerator of roofline.frac.
+def kernel_alu_ops_per_cell(kernel: str):
+    """Generic kernel per u32 (one cell of each of two strips): VIADDMNMX + LOP3 = 2 ALU ops; fp16
+    keys move one row in four's LOP3 to two HADD2s on the FMA pipe (1.75); computed masks add
+    LOP3 + IADD + LOP3 (5).  r = 2 kernel per u32 block of 2 x 2 blown cells x two strips:
+    3 VIMNMX + VIADDMNMX + LOP3 = 5 ALU ops for 8 cells (the ($,$) swap is free; the other
+    mismatch min runs on the FMA pipe).  Large-window kernel: 32-bit keys, one strip per
+    register: VIADDMNMX + LOP3 per cell."""
     if kernel.startswith("comb2"):
-        return peak_ops_clk * 8.0 / 5.0, "r=2 kernel: 5 ALU ops per 8 blown cells"
+        return 5.0 / 8.0, "r=2 kernel: 5 ALU ops per 8 blown cells"
+    if kernel.startswith("combw"):
+        return 2.0, f"large-window kernel {kernel}: 2 ALU ops per cell (32-bit keys)"
     ops = 5.0 if ",computed," in kernel else (1.75 if kernel.endswith("fp16>") else 2.0)
-    return peak_ops_clk * 2.0 / ops, f"generic kernel {kernel}: {ops:g} ALU ops per 2 cells"
+    return ops / 2.0, f"generic kernel {kernel}: {ops:g} ALU ops per 2 cells"
 
 
 def comb_cells(rows, c, n):
     return rows * (c.w * c.r) * (n * c.r)
 
 
-# ---- reference CPU arm ------------------------------------------------------------------------
-def reference_rows_rate(c, x, y, budget_s: float, max_rows: int):
-    """Time the unmodified reference (oracle/_ref) on a bounded, evenly spaced row sample.
+def load_json(path):
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return None
 
-    Returns (rows_done, seconds, cores, sample_desc)."""
+
+# ---- reference CPU arm ------------------------------------------------------------------------
+def reference_rows(c, x, y, budget_s: float, max_rows: int, on_block=None):
+    """Time the unmodified reference (oracle/_ref compute_plot) on a bounded, evenly spaced row sample.
+
+    on_block(row_begin, row_end, grid) is called after each block, outside the timed calls
+    (bench.py's parity check).  Returns (rows_done, seconds, cores, sample_desc) or None."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as ol
 
@@ -165,7 +187,6 @@ def reference_rows_rate(c, x, y, budget_s: float, max_rows: int):
     cores = os.cpu_count() or 1
     mode = ol.SEA8 if c.w <= 254 else ol.SEA16
     rows_total = (x.size - c.w) // c.h + 1
-    # calibrate on a small block
     blk = max(cores, 8)
     t0 = time.perf_counter()
     rc, g, err = ol.ref_plot_rows(x, y, c.w, c.h, c.r, 0, min(blk, rows_total), mode, cores)
@@ -176,15 +197,18 @@ def reference_rows_rate(c, x, y, budget_s: float, max_rows: int):
     nrows = int(min(max_rows, rows_total, max(blk, budget_s / max(per_row, 1e-9))))
     nblocks = max(1, nrows // blk)
     starts = np.linspace(0, rows_total - blk, nblocks).astype(int) if rows_total > blk else [0]
-    done = 0
-    t0 = time.perf_counter()
-    for s in starts:
-        e = min(rows_total, int(s) + blk)
-        rc, g, err = ol.ref_plot_rows(x, y, c.w, c.h, c.r, int(s), e, mode, cores)
+    done, dt = 0, 0.0
+    for s_ in starts:
+        s_ = int(s_)
+        e = min(rows_total, s_ + blk)
+        t0 = time.perf_counter()
+        rc, g, err = ol.ref_plot_rows(x, y, c.w, c.h, c.r, s_, e, mode, cores)
+        dt += time.perf_counter() - t0
         if rc:
             raise RuntimeError(f"reference failed: {err}")
-        done += e - int(s)
-    dt = time.perf_counter() - t0
+        done += e - s_
+        if on_block is not None:
+            on_block(s_, e, g)
     desc = (f"{done} of {rows_total} grid rows ({len(starts)} evenly spaced blocks of {blk}), "
             f"reference compute_plot mode={'sea8' if mode == ol.SEA8 else 'sea16'}, workers={cores}")
     return done, dt, cores, desc
@@ -192,7 +216,7 @@ def reference_rows_rate(c, x, y, budget_s: float, max_rows: int):
 
 def run_reference(args, rank, world):
     # the same workload as the engine arm at this world size (weak scaling grows x), sampled by rows
-    c, x, y = workload(args.config, world)
+    c, x, y = workload(args.config, world, args.scaling)
     rows_total, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
     metric_unit = "window-pair cell updates/s"
     if rank != 0:
@@ -202,22 +226,20 @@ def run_reference(args, rank, world):
     if not ol.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libalignplot_ref.so not built"}))
         return
-    vals = []
     t_all = 0.0
     rows_all = 0
     for _ in range(args.steps):
-        done, dt, cores, desc = reference_rows_rate(c, x, y, budget_s=args.ref_seconds / max(1, args.steps),
-                                                    max_rows=rows_total)
-        vals.append(done * cols * c.w / dt)
+        done, dt, cores, desc = reference_rows(c, x, y, budget_s=args.ref_seconds / max(1, args.steps),
+                                               max_rows=rows_total)
         t_all += dt
         rows_all += done
     value = rows_all * cols * c.w / t_all
     line = {
         "metric": "window-pair cell updates/s (m*n*w/s)", "value": value, "unit": metric_unit,
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * t_all / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000.0 * t_all / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (paper_0909_2000_b200.datagen)",
-        "config": dict(config_desc(c, x, y, world, args.config),
+        "config": dict(config_desc(c, x, y, world, args.config, args.scaling),
                        parallelism=f"reference CPU on rank 0 ({cores} host threads)"),
         "cpu_baseline": {"value": value, "unit": metric_unit, "cores": cores, "kind": "reference",
                          "sample": desc},
@@ -226,12 +248,14 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(c, x, y, world, name):
+def config_desc(c, x, y, world, name, scaling):
     rows, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
+    par = "1 GPU" if world == 1 else (f"row shards x{world} of the fixed plot (w-1 halo)" if scaling == "strong"
+                                      else f"row shards x{world}, x grown x{world} (weak)")
     return {"workload": f"{name}: {c.description}", "m": int(x.size), "n": int(y.size), "w": c.w, "h": c.h,
             "r": c.r, "rows": rows, "cols": cols,
             "output": "dense uint16 half-units" if c.t_half is None else f"threshold half >= {c.t_half}, row-major list",
-            "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+            "parallelism": par,
             "l2": "flushed between steps (256 MiB write, outside the timed events)"}
 
 
@@ -246,7 +270,7 @@ def run_engine(args, rank, world, local_rank):
     local_rank = local_rank % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    c, x, y = workload(args.config, world)
+    c, x, y = workload(args.config, world, args.scaling)
     shard = plan_row_shards(x.size, c.w, c.h, world)[rank]
     xs = shard_x(x, shard)
     n = y.size
@@ -262,31 +286,42 @@ def run_engine(args, rank, world, local_rank):
     d_x = torch.from_numpy(xs.copy()).to(dev)
     d_y = torch.from_numpy(y.copy()).to(dev)
     dense = c.t_half is None
-    cap = 0
-    if dense:
-        d_out = torch.empty(rows_local * cols, dtype=torch.int16, device=dev)
-    else:
-        cap = 1 << 22
-        d_r = torch.empty(cap, dtype=torch.int32, device=dev)
-        d_c = torch.empty(cap, dtype=torch.int32, device=dev)
-        d_h = torch.empty(cap, dtype=torch.int16, device=dev)
     # a dedicated stream: handle 0 would mean "the context's own stream" to the C ABI
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     count = ctypes.c_uint64(0)
+    lists = {}
 
-    def step():
+    def alloc_list(cap):
+        lists["cap"] = cap
+        lists["r"] = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        lists["c"] = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        lists["h"] = torch.empty(max(cap, 1), dtype=torch.int16, device=dev)
+
+    if dense:
+        d_out = torch.empty(rows_local * cols, dtype=torch.int16, device=dev)
+    else:
+        alloc_list(1 << 16)
+
+    def step(strict=True):
         if dense:
             rc = L.ap_ctx_plot_dense_device(ctx, d_x.data_ptr(), xs.size, d_y.data_ptr(), n, ctypes.byref(cfgc),
                                             d_out.data_ptr(), stream.cuda_stream)
         else:
             rc = L.ap_ctx_plot_threshold_device(ctx, d_x.data_ptr(), xs.size, d_y.data_ptr(), n,
-                                                ctypes.byref(cfgc), ctypes.byref(count), d_r.data_ptr(),
-                                                d_c.data_ptr(), d_h.data_ptr(), cap, stream.cuda_stream)
-        if rc not in (0, _native.AP_CAPACITY):
+                                                ctypes.byref(cfgc), ctypes.byref(count), lists["r"].data_ptr(),
+                                                lists["c"].data_ptr(), lists["h"].data_ptr(), lists["cap"],
+                                                stream.cuda_stream)
+            if rc == _native.AP_CAPACITY and not strict:
+                return
+        if rc:
             raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
 
+    # the first call sizes the device list; every timed step then places the whole list
+    step(strict=False)
+    if not dense and count.value > lists["cap"]:
+        alloc_list(int(count.value))
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -328,9 +363,16 @@ def run_engine(args, rank, world, local_rank):
         gathered = [torch.zeros_like(cnt_t) for _ in range(world)]
         dist.all_gather(gathered, cnt_t)
         hits_all = [int(g_.item()) for g_ in gathered]
+    # what the last timed step produced (parity below)
+    if dense:
+        last_out = d_out.cpu().numpy().view(np.uint16).reshape(rows_local, cols)
+    else:
+        k = hits_local
+        last_list = (lists["r"][:k].cpu().numpy().view(np.uint32), lists["c"][:k].cpu().numpy().view(np.uint32),
+                     lists["h"][:k].cpu().numpy().view(np.int16).astype(np.int32))
 
     # ---- end to end through the public host API (pinned host buffers) ----
-    hx = torch.from_numpy(xs.copy()).pin_memory()
+    hx = torch.from_numpy(x.copy()).pin_memory()
     hy = torch.from_numpy(y.copy()).pin_memory()
     cfg_py = ap.PlotConfig(window_w=c.w, step_h=c.h, blowup_r=c.r, threshold_half=c.t_half, mode=ap.Mode.cuda)
     if dense:
@@ -340,13 +382,14 @@ def run_engine(args, rank, world, local_rank):
         hr = torch.empty(cap_h, dtype=torch.int32).pin_memory()
         hc = torch.empty(cap_h, dtype=torch.int32).pin_memory()
         hh = torch.empty(cap_h, dtype=torch.int16).pin_memory()
-    apc = ap._cfg(cfg_py)
+    # this rank's rows of the plot of (x, y): the host API uploads only their x bytes (+ halo)
+    apc = ap._cfg(cfg_py, shard.row_begin, shard.row_end)
 
     def e2e_step():
         if dense:
-            rc = L.ap_plot_dense(hx.data_ptr(), xs.size, hy.data_ptr(), n, ctypes.byref(apc), hout.data_ptr())
+            rc = L.ap_plot_dense(hx.data_ptr(), x.size, hy.data_ptr(), n, ctypes.byref(apc), hout.data_ptr())
         else:
-            rc = L.ap_plot_threshold(hx.data_ptr(), xs.size, hy.data_ptr(), n, ctypes.byref(apc), ctypes.byref(count),
+            rc = L.ap_plot_threshold(hx.data_ptr(), x.size, hy.data_ptr(), n, ctypes.byref(apc), ctypes.byref(count),
                                      hr.data_ptr(), hc.data_ptr(), hh.data_ptr(), cap_h)
         if rc:
             raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
@@ -365,13 +408,14 @@ def run_engine(args, rank, world, local_rank):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te[0])
     d2h = rows_local * cols * 2 if dense else hits_local * 10 + 8
+    h2d = (shard.x_end - shard.x_begin) + n
     # the same through ap_plot_dense_u8 (lossless bytes for w <= 127): half the D2H
     e2e_u8 = None
     if dense and c.w <= 127:
         hout8 = torch.empty(rows_local * cols, dtype=torch.uint8).pin_memory()
 
         def e2e_u8_step():
-            rc = L.ap_plot_dense_u8(hx.data_ptr(), xs.size, hy.data_ptr(), n, ctypes.byref(apc), hout8.data_ptr())
+            rc = L.ap_plot_dense_u8(hx.data_ptr(), x.size, hy.data_ptr(), n, ctypes.byref(apc), hout8.data_ptr())
             if rc:
                 raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
 
@@ -385,7 +429,7 @@ def run_engine(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(te8, op=dist.ReduceOp.MAX)
         e2e_u8 = {"value": rows_global * cols * c.w * args.steps / float(te8[0]), "unit": "window-pair cell updates/s",
-                  "h2d_bytes_per_step": int(xs.size + n), "d2h_bytes_per_step": int(rows_local * cols),
+                  "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(rows_local * cols),
                   "api": "ap_plot_dense_u8 (half-unit scores as bytes, lossless for w <= 127)"}
 
     if rank != 0:
@@ -395,61 +439,88 @@ def run_engine(args, rank, world, local_rank):
     value = wpcu * args.steps / t_max
     clocks = clk.summary()
     cells_local = comb_cells(rows_local, c, n)
-    peak_ops_clk = None
-    if os.path.exists(INT_PEAK):
-        with open(INT_PEAK) as f:
-            peak_ops_clk = json.load(f).get("lane_ops_per_clk_per_sm")
+    int_peak = load_json(INT_PEAK) or {}
+    peak_ops_clk = int_peak.get("lane_ops_per_clk_per_sm")
     sm_mhz = clocks["sm_mhz"] or 1965.0
     props = torch.cuda.get_device_properties(dev)
     roof = None
     if peak_ops_clk:
-        peak = props.multi_processor_count * peak_ops_clk * sm_mhz * 1e6 / 1e12
-        achieved = cells_local * 3 / kern_max / 1e12
-        traffic = None
-        if os.path.exists(NCU_TRAFFIC):
-            with open(NCU_TRAFFIC) as f:
-                traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
-        cpc = cells_local / kern_max / (props.multi_processor_count * sm_mhz * 1e6)
-        ceiling, ceiling_what = kernel_ceiling(kernel, peak_ops_clk)
-        roof = {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
+        peak = props.multi_processor_count * peak_ops_clk * sm_mhz * 1e6 / 1e12   # T lane-ops/s
+        ops_cell, ops_what = kernel_alu_ops_per_cell(kernel)
+        achieved = cells_local * ops_cell / kern_max / 1e12
+        traffic = ((load_json(NCU_TRAFFIC) or {}).get(args.config) or {}).get("dram_bytes_per_launch")
+        roof = {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "T ALU lane-ops/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel_alu_bound": {"kernel": kernel, "cells_per_clk_per_sm": cpc, "ceiling": ceiling,
-                                     "frac": cpc / ceiling,
-                                     "what": "comb cells per SM clock vs this kernel's own ALU-pipe instruction "
-                                             "ceiling at the measured rate: " + ceiling_what},
-                "basis": "3 int32 lane-ops per comb cell (SURVEY §8d), cells = rows*(w*r)*(n*r); peak = "
-                         f"{props.multi_processor_count} SMs x {peak_ops_clk:.1f} measured lane-ops/clk/SM x "
-                         f"{sm_mhz:.0f} MHz (median SM clock during the run)",
-                "kernel_ms": kern_max * 1000.0, "comb_cells_per_s": cells_local / kern_max}
-    hbm = None
-    if os.path.exists(MEASURED_PEAKS):
-        with open(MEASURED_PEAKS) as f:
-            hbm_peak = json.load(f).get("hbm_gbs")
-        out_bytes = rows_local * cols * 2 if dense else hits_local * 10 + 8
-        hbm = {"bound": "hbm", "achieved": out_bytes / kern_max / 1e9, "peak": hbm_peak, "unit": "GB/s",
-               "frac": out_bytes / kern_max / 1e9 / hbm_peak if hbm_peak else None,
-               "what": "plot output stream written by the comb kernel"}
+                "what": f"the comb kernel's own ALU instructions ({ops_what}) x comb cells / kernel time, against "
+                        f"the measured ALU-pipe issue peak: {props.multi_processor_count} SMs x "
+                        f"{peak_ops_clk:.1f} lane-ops/clk/SM (profiles/int_peak_r01.json) x {sm_mhz:.0f} MHz "
+                        "(median SM clock during the timed region)",
+                "kernel": kernel, "kernel_ms": kern_max * 1000.0, "comb_cells_per_s": cells_local / kern_max,
+                # SURVEY §8d's fixed basis: the reference recurrence at 3 int32 lane-ops per comb cell.
+                # Above 1 = the kernel does less ALU work per cell than that recurrence, not faster
+                # than the hardware.
+                "vs_generic_recurrence": cells_local * 3.0 / kern_max / 1e12 / peak}
+    hbm_peak = (load_json(MEASURED_PEAKS) or {}).get("hbm_gbs")
+    out_bytes = rows_local * cols * 2 if dense else hits_local * 10 + 8
+    hbm = {"bound": "hbm", "achieved": out_bytes / kern_max / 1e9, "peak": hbm_peak, "unit": "GB/s",
+           "frac": out_bytes / kern_max / 1e9 / hbm_peak if hbm_peak else None,
+           "what": "plot output stream written by the comb kernel"}
 
-    cpu = None
+    # ---- CPU baseline (the unmodified reference) and parity of the timed output on its rows ----
+    cpu, parity = None, None
     if world == 1 and not args.no_cpu_baseline:
-        res = reference_rows_rate(c, x, y, budget_s=args.ref_seconds, max_rows=rows_global)
+        par = {"rows": 0, "dense_mismatches": 0, "list_cells": 0, "list_mismatches": 0}
+        dense_buf = None
+
+        def check_block(rb, re, g):
+            nonlocal dense_buf
+            par["rows"] += re - rb
+            if dense:
+                par["dense_mismatches"] += int(np.count_nonzero(last_out[rb:re].astype(np.int32) != g))
+                return
+            # the timed list restricted to these rows vs apply_threshold of the reference rows
+            lr, lc, lh = last_list
+            i0, i1 = np.searchsorted(lr, rb), np.searchsorted(lr, re)
+            er, ec = np.nonzero(g >= c.t_half)
+            got = (lr[i0:i1].astype(np.int64) - rb, lc[i0:i1].astype(np.int64), lh[i0:i1])
+            same = (got[0].size == er.size and np.array_equal(got[0], er) and np.array_equal(got[1], ec)
+                    and np.array_equal(got[2], g[er, ec]))
+            par["list_cells"] += int(er.size)
+            par["list_mismatches"] += 0 if same else max(1, abs(int(got[0].size) - int(er.size)))
+            # and the dense scores of the same rows (device API, row range)
+            cb = _native.ApConfig(window_w=c.w, step_h=c.h, blowup_r=c.r, has_threshold=0, threshold_half=0,
+                                  n_devices=1, row_begin=rb, row_end=re)
+            if dense_buf is None or dense_buf.numel() < (re - rb) * cols:
+                dense_buf = torch.empty((re - rb) * cols, dtype=torch.int16, device=dev)
+            rc = L.ap_ctx_plot_dense_device(ctx, d_x.data_ptr(), xs.size, d_y.data_ptr(), n, ctypes.byref(cb),
+                                            dense_buf.data_ptr(), stream.cuda_stream)
+            if rc:
+                raise RuntimeError(f"engine status {rc}: {_native.last_error()}")
+            gd = dense_buf[:(re - rb) * cols].cpu().numpy().view(np.uint16).reshape(re - rb, cols)
+            par["dense_mismatches"] += int(np.count_nonzero(gd.astype(np.int32) != g))
+
+        res = reference_rows(c, x, y, budget_s=args.ref_seconds, max_rows=rows_global, on_block=check_block)
         if res:
             done, dt, cores, desc = res
             cpu = {"value": done * cols * c.w / dt, "unit": "window-pair cell updates/s", "cores": cores,
                    "kind": "reference", "sample": desc}
+            parity = dict(par, against="oracle/_ref (unmodified reference compute_plot) on the cpu_baseline rows",
+                          what="dense: the timed plot's rows; threshold: the timed list restricted to those rows "
+                               "(+ the device API's dense scores of the same rows)")
     line = {
         "metric": "window-pair cell updates/s (m*n*w/s)", "value": value, "unit": "window-pair cell updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u16",
         "data": "synthetic (seeded, paper_0909_2000_b200.datagen)",
-        "config": config_desc(c, x, y, world, args.config),
+        "config": config_desc(c, x, y, world, args.config, args.scaling),
         "entries_per_s": rows_global * cols * args.steps / t_max,
         "comb_cells_per_s": comb_cells(rows_global, c, n) * args.steps / t_max,
         "roofline": roof, "roofline_hbm_output": hbm, "clocks": clocks,
         "e2e": {"value": wpcu * args.steps / t_e2e, "unit": "window-pair cell updates/s",
-                "h2d_bytes_per_step": int(xs.size + n), "d2h_bytes_per_step": int(d2h)},
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "ap_plot_dense" if dense else "ap_plot_threshold (pinned host arrays sized by the count)"},
         "e2e_compact": e2e_u8,
-        "gpu_launches": launches, "kernel": kernel, "cpu_baseline": cpu,
+        "gpu_launches": launches, "kernel": kernel, "cpu_baseline": cpu, "parity": parity,
     }
     if not dense:
         line["hits_rank0"] = hits_local
@@ -462,15 +533,20 @@ def run_engine(args, rank, world, local_rank):
 def main():
     ap_ = argparse.ArgumentParser()
     ap_.add_argument("--gpus", type=int, default=1)
-    ap_.add_argument("--steps", type=int, default=30)
-    ap_.add_argument("--warmup", type=int, default=5)
-    ap_.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS))
+    ap_.add_argument("--steps", type=int, default=10)
+    ap_.add_argument("--warmup", type=int, default=3)
+    ap_.add_argument("--config", default="C4", choices=sorted(datagen.CONFIGS))
+    ap_.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                     help="strong: shard the config's fixed plot over the ranks (default for C4, C5); "
+                          "weak: grow x with the rank count (default for C1-C3)")
     ap_.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap_.add_argument("--ref-seconds", type=float, default=8.0, help="wall-clock budget of the CPU reference sample")
     ap_.add_argument("--no-cpu-baseline", action="store_true")
     ap_.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                      help="gloo: exercise the N>1 code path with several ranks on one GPU (timing not meaningful)")
     args = ap_.parse_args()
+    if args.scaling is None:
+        args.scaling = default_scaling(args.config)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -82,6 +82,17 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
                       uint64_t* count, uint32_t* rows, uint32_t* cols, uint16_t* halves,
                       size_t cap);
 
+/* Single-pass form of ap_plot_threshold for callers that cannot size the list in
+ * advance (apply_threshold returns a vector of exactly the passing cells,
+ * scoring.cpp:30-39): the plot is combed once; when the total is known the
+ * engine calls alloc(user, count, &rows, &cols, &halves) exactly once (also for
+ * count 0) to get host arrays of at least `count` entries, then writes the
+ * row-major list into them.  A nonzero return from alloc aborts with AP_INVALID. */
+typedef int (*ap_list_alloc_fn)(void* user, uint64_t count, uint32_t** rows, uint32_t** cols,
+                                uint16_t** halves);
+int ap_plot_threshold_into(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                           ap_list_alloc_fn alloc, void* user, uint64_t* count);
+
 /* One thresholded cell (PlotCell, scoring.hpp:33-42) for the array-of-structs
  * form below. */
 typedef struct ap_cell {

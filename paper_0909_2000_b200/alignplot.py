@@ -311,26 +311,45 @@ def compute_plot(x: Sequence, y: Sequence, cfg: PlotConfig) -> PlotGrid:
 
 def plot_threshold_arrays(x, y, cfg: PlotConfig, t_half: int, cap: Optional[int] = None,
                           row_begin: int = 0, row_end: int = 0):
-    """Fused threshold + row-major compaction via ap_plot_threshold: (rows, cols, halves) arrays."""
+    """Fused threshold + row-major compaction: (rows, cols, halves) arrays.
+
+    One comb of the plot: through ap_plot_threshold_into, whose callback allocates the arrays
+    once the count is known (apply_threshold's exact-size result, scoring.cpp:30-39).  With an
+    explicit ``cap`` the fixed-capacity entry ap_plot_threshold is used instead; a longer list
+    raises ``EngineError`` (AP_CAPACITY)."""
     xa, ya = _codes(x), _codes(y)
     c = _cfg(cfg, row_begin, row_end)
     c.has_threshold = 1
     c.threshold_half = int(t_half)
     L = _native.lib()
     count = ctypes.c_uint64(0)
-    cap0 = 1 << 16 if cap is None else cap
-    while True:
-        r = np.empty(cap0, dtype=np.uint32)
-        k = np.empty(cap0, dtype=np.uint32)
-        hv = np.empty(cap0, dtype=np.uint16)
-        rc = L.ap_plot_threshold(_ptr(xa), xa.size, _ptr(ya), ya.size, ctypes.byref(c), ctypes.byref(count),
-                                 _ptr(r), _ptr(k), _ptr(hv), cap0)
-        if rc == _native.AP_CAPACITY and cap is None:
-            cap0 = int(count.value)
-            continue
-        _raise(rc)
+    if cap is not None:
+        r = np.empty(cap, dtype=np.uint32)
+        k = np.empty(cap, dtype=np.uint32)
+        hv = np.empty(cap, dtype=np.uint16)
+        _raise(L.ap_plot_threshold(_ptr(xa), xa.size, _ptr(ya), ya.size, ctypes.byref(c), ctypes.byref(count),
+                                   _ptr(r), _ptr(k), _ptr(hv), cap))
         n = int(count.value)
         return r[:n], k[:n], hv[:n]
+    held = {}
+
+    def alloc(_user, n, pr, pc, ph):
+        try:
+            held["r"] = np.empty(max(int(n), 1), dtype=np.uint32)
+            held["c"] = np.empty(max(int(n), 1), dtype=np.uint32)
+            held["h"] = np.empty(max(int(n), 1), dtype=np.uint16)
+        except MemoryError:
+            return 1
+        pr[0] = held["r"].ctypes.data
+        pc[0] = held["c"].ctypes.data
+        ph[0] = held["h"].ctypes.data
+        return 0
+
+    cb = _native.ListAllocFn(alloc)
+    _raise(L.ap_plot_threshold_into(_ptr(xa), xa.size, _ptr(ya), ya.size, ctypes.byref(c), cb, None,
+                                    ctypes.byref(count)))
+    n = int(count.value)
+    return held["r"][:n], held["c"][:n], held["h"][:n]
 
 
 def plot_threshold_cells(x, y, cfg: PlotConfig, t_half: int, row_begin: int = 0, row_end: int = 0) -> List[PlotCell]:

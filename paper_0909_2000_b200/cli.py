@@ -5,7 +5,8 @@
          [--bench --modes dp,sea8]
 
 Same flags, defaults and output bytes as the reference.  Every --mode runs on the
-GPU (the reference's engines agree bit for bit); thresholded TSV/dots come from
+GPU (the reference's engine names are aliases of the CUDA engine: its engines agree bit
+for bit, acceptance.cpp:34-73; --bench reports the aliasing); thresholded TSV/dots come from
 the fused threshold+compact kernel and PGM pixels from the fused quantiser, so no
 dense grid is materialised for them.
 """
@@ -32,11 +33,20 @@ def _llround(v: float) -> int:
 
 
 def benchmark(x: ap.Sequence, y: ap.Sequence, cfg: ap.PlotConfig, modes: List[ap.Mode]) -> dict:
-    """io.cpp:192-233: time each mode, insist the grids agree, Mcups normalised to the DP cost."""
+    """The shape of io.cpp:192-233 (time each requested mode; Mcups normalised to the DP cost
+    rows*cols*(w*r)^2), on this engine.
+
+    The reference races different engines and insists their grids agree.  Here every mode is
+    served by the one CUDA engine -- dp / blcs / sea_scalar / sea16 / sea8 are aliases of
+    ``cuda`` (each entry says so in ``engine``) -- so that check cannot compare engines; what
+    it checks instead is run-to-run determinism of the engine (bitwise-identical grids), and
+    the report says which it was.  Cross-engine agreement with the reference is the job of the
+    parity tests (tests/test_gpu_parity.py against oracle/_ref)."""
     if not modes:
         raise ap.ConfigError("benchmark needs at least one mode")
     rep = {"rows": 0, "cols": 0, "window": cfg.window_w, "step": cfg.step_h, "blowup": cfg.blowup_r,
-           "workers": cfg.workers, "results": []}
+           "workers": cfg.workers, "results": [],
+           "agreement_check": "run-to-run determinism of the CUDA engine (every mode is an alias of cuda)"}
     reference = None
     for m in modes:
         c = ap.PlotConfig(**{**cfg.__dict__, "mode": m})
@@ -47,25 +57,25 @@ def benchmark(x: ap.Sequence, y: ap.Sequence, cfg: ap.PlotConfig, modes: List[ap
             reference = grid
             rep["rows"], rep["cols"] = grid.rows, grid.cols
         elif grid != reference:
-            raise RuntimeError(f"benchmark: mode {m.name} disagrees with {modes[0].name}")
+            raise RuntimeError(f"benchmark: run for mode {m.name} is not bitwise identical to the first run")
         wr = float(cfg.window_w * cfg.blowup_r)
         cells = float(rep["rows"]) * float(rep["cols"]) * wr * wr
         first = rep["results"][0]["seconds"] if rep["results"] else secs
-        rep["results"].append({"mode": m.name, "seconds": secs, "cell_updates_per_sec": cells / secs,
+        rep["results"].append({"mode": m.name, "engine": "cuda", "seconds": secs, "cell_updates_per_sec": cells / secs,
                                "speedup_vs_first": first / secs})
     return rep
 
 
 def bench_text(rep: dict) -> str:
-    """BenchReport::to_text (io.cpp:155-174)."""
+    """BenchReport::to_text layout (io.cpp:155-174), plus the engine each mode ran on."""
     out = [f"plot {rep['rows']} x {rep['cols']} windows, w={rep['window']}, h={rep['step']}, "
            f"r={rep['blowup']}, workers={rep['workers']}",
-           f"{'mode':<12} {'seconds':>10} {'Mcups':>12} {'speedup':>9}"]
+           f"{'mode':<12} {'seconds':>10} {'Mcups':>12} {'speedup':>9}  engine"]
     for e in rep["results"]:
         out.append(f"{e['mode']:<12} {e['seconds']:10.3f} {e['cell_updates_per_sec'] / 1e6:12.1f} "
-                   f"{e['speedup_vs_first']:8.2f}x")
-    if any(e["mode"] == "dp" for e in rep["results"]):
-        out.append("dp = exhaustive per-window DP baseline, no shortcuts")
+                   f"{e['speedup_vs_first']:8.2f}x  {e['engine']}")
+    out.append("every mode runs on the CUDA engine (the reference's engine names are aliases); "
+               "agreement = run-to-run determinism")
     return "\n".join(out) + "\n"
 
 

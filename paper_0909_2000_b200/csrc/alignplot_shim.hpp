@@ -8,26 +8,22 @@
 //   runner.hpp   StripTask, plan_strips, compute_plot
 //   scoring.hpp  BlownSequence, blowup, unblow, recover_score, PlotCell,
 //                apply_threshold
-// so code written against the reference compiles unchanged and links
-// libalignplot_b200.so instead.  compute_plot runs on the CUDA engine through
+// so hot-path code written against the reference compiles unchanged and links
+// libalignplot_b200.so instead.  The reference's io layer (FASTA, writers,
+// benchmark; io.hpp) is not mirrored: plot output comes from the device as
+// write_{tsv,dots,pgm}_gpu below (same bytes as io.cpp:102-153).  compute_plot runs on the CUDA engine through
 // the C ABI (include/alignplot_b200.h) for every Mode: the reference proves all
 // its engines produce the identical grid (tests/acceptance.cpp:34-73), while
 // PlotConfig::validate keeps each mode's limits.  Extras: Mode::cuda,
-// PlotConfig::n_devices, and compute_plot_threshold (fused threshold +
-// row-major compaction without a dense grid).
+// PlotConfig::n_devices, compute_plot_threshold (fused threshold + row-major
+// compaction without a dense grid) and the GPU-fed writers.
 #pragma once
 
 #include <algorithm>
-#include <chrono>
-#include <cmath>
+#include <charconv>
 #include <cstdint>
-#include <cstdlib>
-#include <cstdio>
-#include <fstream>
-#include <istream>
 #include <optional>
 #include <ostream>
-#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -51,11 +47,6 @@ class EmptyPlotError : public ConfigError {
   explicit EmptyPlotError(const std::string& what) : ConfigError(what) {}
 };
 
-class ParseError : public std::runtime_error {
- public:
-  explicit ParseError(const std::string& what) : std::runtime_error(what) {}
-};
-
 // No CUDA device or a CUDA runtime failure: the engine has no CPU fallback.
 class EngineError : public std::runtime_error {
  public:
@@ -74,43 +65,6 @@ inline void check(int rc) {
     case AP_INVALID: throw std::invalid_argument(msg);
     default: throw EngineError("alignplot_b200 status " + std::to_string(rc) + ": " + msg);
   }
-}
-// A double as the reference's JSON writer prints it: the shortest digit string
-// that round-trips, in fixed notation (with a trailing ".0" when integral) for
-// values in [1e-4, 1e15), scientific ("1.5e+20", "1e-05") outside.
-inline std::string json_double(double v) {
-  if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
-  char buf[64];
-  int p = 0;
-  for (; p < 17; ++p) {   // shortest round-trip mantissa
-    std::snprintf(buf, sizeof buf, "%.*e", p, v);
-    if (std::strtod(buf, nullptr) == v) break;
-  }
-  std::snprintf(buf, sizeof buf, "%.*e", p, v);
-  std::string m(buf);
-  const bool neg = m[0] == '-';
-  if (neg) m.erase(0, 1);
-  const std::size_t epos = m.find('e');
-  const int e10 = std::atoi(m.c_str() + epos + 1);
-  std::string d;
-  for (std::size_t i = 0; i < epos; ++i)
-    if (m[i] != '.') d.push_back(m[i]);
-  while (d.size() > 1 && d.back() == '0') d.pop_back();
-  const int k = int(d.size()), n = e10 + 1;   // value = 0.d * 10^n
-  std::string out;
-  if (k <= n && n <= 15) {
-    out = d + std::string(size_t(n - k), '0') + ".0";
-  } else if (0 < n && n <= 15) {
-    out = d.substr(0, size_t(n)) + "." + d.substr(size_t(n));
-  } else if (-4 < n && n <= 0) {
-    out = "0." + std::string(size_t(-n), '0') + d;
-  } else {
-    const int x = n - 1;
-    char eb[16];
-    std::snprintf(eb, sizeof eb, "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
-    out = (k == 1 ? d : d.substr(0, 1) + "." + d.substr(1)) + eb;
-  }
-  return neg ? "-" + out : out;
 }
 }  // namespace detail
 
@@ -320,76 +274,138 @@ inline std::vector<PlotCell> apply_threshold(const PlotGrid& grid, half_score_t 
 }
 
 // apply_threshold(compute_plot(x, y, cfg), t) fused on the GPU: no dense grid
-// is materialised; cells come back in the same row-major order.
+// is materialised; cells come back in the same row-major order.  One comb: the
+// engine sizes the result through ap_plot_threshold_into's callback.
 inline std::vector<PlotCell> compute_plot_threshold(const Sequence& x, const Sequence& y, const PlotConfig& cfg,
                                                     half_score_t t_half) {
   cfg.validate(x.size(), y.size());
   PlotConfig tc = cfg;
   tc.threshold_half = t_half;
   const ap_config c = tc.to_c();
+  struct Lists {
+    std::vector<std::uint32_t> r, c;
+    std::vector<std::uint16_t> h;
+  } lists;
+  auto alloc = [](void* user, std::uint64_t count, std::uint32_t** rows, std::uint32_t** cols,
+                  std::uint16_t** halves) -> int {
+    auto* l = static_cast<Lists*>(user);
+    l->r.resize(count);
+    l->c.resize(count);
+    l->h.resize(count);
+    *rows = l->r.data();
+    *cols = l->c.data();
+    *halves = l->h.data();
+    return 0;
+  };
   std::uint64_t count = 0;
-  std::vector<std::uint32_t> rr(1 << 12), cc(1 << 12);
-  std::vector<std::uint16_t> hh(1 << 12);
-  int rc = ap_plot_threshold(x.data.data(), x.size(), y.data.data(), y.size(), &c, &count, rr.data(),
-                             cc.data(), hh.data(), rr.size());
-  if (rc == AP_CAPACITY) {
-    rr.resize(count);
-    cc.resize(count);
-    hh.resize(count);
-    rc = ap_plot_threshold(x.data.data(), x.size(), y.data.data(), y.size(), &c, &count, rr.data(),
-                           cc.data(), hh.data(), rr.size());
-  }
-  detail::check(rc);
+  detail::check(ap_plot_threshold_into(x.data.data(), x.size(), y.data.data(), y.size(), &c, alloc, &lists, &count));
   std::vector<PlotCell> out(count);
-  for (std::size_t k = 0; k < count; ++k) out[k] = {rr[k], cc[k], hh[k]};
+  for (std::size_t k = 0; k < count; ++k)
+    out[k] = {lists.r[k], lists.c[k], static_cast<half_score_t>(static_cast<std::int16_t>(lists.h[k]))};
   return out;
 }
 
-// ---- writers (io.cpp:102-153), byte-identical ------------------------------
-inline std::string half_to_decimal(half_score_t half) {
-  const bool neg = half < 0;
-  const long long a = neg ? -static_cast<long long>(half) : half;
-  std::string out = neg ? "-" : "";
-  out += std::to_string(a / 2);
-  out += (a % 2) ? ".5" : ".0";
-  return out;
+// ---- GPU-fed plot output ------------------------------------------------------
+// The reference writes its three formats from a materialised PlotGrid (io.cpp:102-153).
+// Here the device produces what each format needs -- the thresholded row-major list for
+// sparse TSV / dot output, quantised pixels for PGM (ap_plot_pgm), dense row blocks
+// otherwise -- and the host only formats bytes.  The bytes equal the reference writers'
+// (tests/golden/cli, tests/cpp/test_shim.cpp).
+namespace detail {
+// "<a> <sep> <b> <sep> <half as decimal>" with the half-unit score printed as k.0 / k.5
+inline char* put_half(char* p, half_score_t half) {
+  if (half < 0) *p++ = '-';
+  const std::uint64_t mag = half < 0 ? std::uint64_t(-std::int64_t(half)) : std::uint64_t(half);
+  p = std::to_chars(p, p + 24, mag >> 1).ptr;
+  *p++ = '.';
+  *p++ = (mag & 1) ? '5' : '0';
+  return p;
 }
 
-inline void write_tsv(std::ostream& out, const PlotGrid& grid, std::optional<half_score_t> threshold_half,
-                      bool dense) {
-  out << "# x_offset y_offset score\n";
-  for (std::size_t r = 0; r < grid.rows; ++r)
-    for (std::size_t c = 0; c < grid.cols; ++c) {
-      const half_score_t v = grid.at(r, c);
-      if (!dense && threshold_half && v < *threshold_half) continue;
-      out << grid.x_offset(r) << '\t' << grid.y_offset(c) << '\t' << half_to_decimal(v) << '\n';
-    }
+// A buffered sink: format into a local block, hand full blocks to the stream.
+struct LineSink {
+  std::ostream& out;
+  std::vector<char> buf = std::vector<char>(size_t(1) << 20);
+  std::size_t used = 0;
+  explicit LineSink(std::ostream& o) : out(o) {}
+  char* reserve(std::size_t n) {
+    if (used + n > buf.size()) flush();
+    return buf.data() + used;
+  }
+  void commit(char* end) { used = std::size_t(end - buf.data()); }
+  void flush() {
+    out.write(buf.data(), static_cast<std::streamsize>(used));
+    used = 0;
+  }
+};
+
+// (row offset, col offset[, score]) lines of the cells passing the threshold, from the list
+template <typename Emit>
+inline void for_list(const Sequence& x, const Sequence& y, const PlotConfig& cfg, half_score_t t, Emit emit) {
+  for (const PlotCell& cell : compute_plot_threshold(x, y, cfg, t)) emit(cell.row, cell.col, cell.score_half);
+}
+
+// every cell, from dense row blocks of about 64 MiB (bounded host memory for any plot size)
+template <typename Emit>
+inline void for_dense(const Sequence& x, const Sequence& y, const PlotConfig& cfg, Emit emit) {
+  const auto [rows, cols] = window_grid_dims(x.size(), y.size(), cfg.window_w, cfg.step_h);
+  PlotConfig dc = cfg;
+  dc.threshold_half.reset();
+  const std::size_t block = std::max<std::size_t>(1, (std::size_t(32) << 20) / std::max<std::size_t>(cols, 1));
+  std::vector<std::uint16_t> half;
+  for (std::size_t r0 = 0; r0 < rows; r0 += block) {
+    const std::size_t r1 = std::min(rows, r0 + block);
+    half.resize((r1 - r0) * cols);
+    const ap_config c = dc.to_c(r0, r1);
+    check(ap_plot_dense(x.data.data(), x.size(), y.data.data(), y.size(), &c, half.data()));
+    for (std::size_t r = r0; r < r1; ++r)
+      for (std::size_t k = 0; k < cols; ++k)
+        emit(r, k, static_cast<half_score_t>(static_cast<std::int16_t>(half[(r - r0) * cols + k])));
+  }
+}
+}  // namespace detail
+
+// TSV of compute_plot(x, y, cfg): header line, then "x_offset\ty_offset\tscore" per cell;
+// without `dense`, only cells passing cfg.threshold_half (io.cpp:102-119 semantics).
+inline void write_tsv_gpu(std::ostream& out, const Sequence& x, const Sequence& y, const PlotConfig& cfg,
+                          bool dense) {
+  cfg.validate(x.size(), y.size());
+  detail::LineSink sink(out);
+  const std::string head = "# x_offset y_offset score\n";
+  char* p = sink.reserve(head.size());
+  sink.commit(std::copy(head.begin(), head.end(), p));
+  auto emit = [&](std::size_t r, std::size_t c, half_score_t v) {
+    char* q = sink.reserve(64);
+    q = std::to_chars(q, q + 24, r * cfg.step_h).ptr;
+    *q++ = '\t';
+    q = std::to_chars(q, q + 24, c).ptr;
+    *q++ = '\t';
+    q = detail::put_half(q, v);
+    *q++ = '\n';
+    sink.commit(q);
+  };
+  if (!dense && cfg.threshold_half) detail::for_list(x, y, cfg, *cfg.threshold_half, emit);
+  else detail::for_dense(x, y, cfg, emit);
+  sink.flush();
   if (!out) throw std::runtime_error("write failure on TSV sink");
 }
 
-inline void write_dots(std::ostream& out, const PlotGrid& grid, std::optional<half_score_t> threshold_half) {
-  for (std::size_t r = 0; r < grid.rows; ++r)
-    for (std::size_t c = 0; c < grid.cols; ++c) {
-      if (threshold_half && grid.at(r, c) < *threshold_half) continue;
-      out << grid.x_offset(r) << ' ' << grid.y_offset(c) << '\n';
-    }
+// "x_offset y_offset" per cell passing cfg.threshold_half (every cell without one; io.cpp:121-133).
+inline void write_dots_gpu(std::ostream& out, const Sequence& x, const Sequence& y, const PlotConfig& cfg) {
+  cfg.validate(x.size(), y.size());
+  detail::LineSink sink(out);
+  auto emit = [&](std::size_t r, std::size_t c, half_score_t) {
+    char* q = sink.reserve(64);
+    q = std::to_chars(q, q + 24, r * cfg.step_h).ptr;
+    *q++ = ' ';
+    q = std::to_chars(q, q + 24, c).ptr;
+    *q++ = '\n';
+    sink.commit(q);
+  };
+  if (cfg.threshold_half) detail::for_list(x, y, cfg, *cfg.threshold_half, emit);
+  else detail::for_dense(x, y, cfg, emit);
+  sink.flush();
   if (!out) throw std::runtime_error("write failure on dot sink");
-}
-
-inline void write_pgm(std::ostream& out, const PlotGrid& grid, std::optional<half_score_t> threshold_half) {
-  out << "P5\n" << grid.cols << ' ' << grid.rows << "\n255\n";
-  const long long full = 2 * static_cast<long long>(grid.window_w);
-  std::vector<unsigned char> row(grid.cols);
-  for (std::size_t r = 0; r < grid.rows; ++r) {
-    for (std::size_t c = 0; c < grid.cols; ++c) {
-      half_score_t v = grid.at(r, c);
-      if (threshold_half && v < *threshold_half) v = 0;
-      const long long h = std::clamp<long long>(v, 0, full);
-      row[c] = static_cast<unsigned char>((255 * h + full / 2) / full);
-    }
-    out.write(reinterpret_cast<const char*>(row.data()), static_cast<std::streamsize>(row.size()));
-  }
-  if (!out) throw std::runtime_error("write failure on PGM sink");
 }
 
 // The PGM of compute_plot(x, y, cfg) without a dense grid on the host: pixels
@@ -403,155 +419,6 @@ inline void write_pgm_gpu(std::ostream& out, const Sequence& x, const Sequence& 
   out << "P5\n" << cols << ' ' << rows << "\n255\n";
   out.write(reinterpret_cast<const char*>(pix.data()), static_cast<std::streamsize>(pix.size()));
   if (!out) throw std::runtime_error("write failure on PGM sink");
-}
-
-// ---- FASTA input (io.hpp:15-38, io.cpp:32-100) ----------------------------
-struct FastaRecord {
-  std::string header;
-  std::string sequence;
-  bool operator==(const FastaRecord&) const = default;
-};
-
-inline std::vector<FastaRecord> read_fasta_stream(std::istream& in, const std::string& source) {
-  std::vector<FastaRecord> recs;
-  std::size_t line_no = 0, header_line = 0;
-  auto fail = [&](std::size_t ln, const std::string& what) {
-    throw ParseError(source + ":" + std::to_string(ln) + ": " + what);
-  };
-  auto space = [](unsigned char c) { return c == ' ' || (c >= '\t' && c <= '\r'); };
-  std::string line;
-  while (std::getline(in, line)) {
-    ++line_no;
-    if (!line.empty() && line.back() == '\r') line.pop_back();
-    if (std::all_of(line.begin(), line.end(), [&](char c) { return space(static_cast<unsigned char>(c)); }))
-      continue;   // empty or blank
-    if (line[0] == '>') {
-      if (!recs.empty() && recs.back().sequence.empty())
-        fail(header_line, "record '" + recs.back().header + "' has no sequence data");
-      std::size_t e = line.size();
-      while (e > 1 && space(static_cast<unsigned char>(line[e - 1]))) --e;
-      recs.push_back({line.substr(1, e - 1), {}});
-      header_line = line_no;
-      continue;
-    }
-    if (recs.empty()) fail(line_no, "sequence data before first header");
-    for (char ch : line) {
-      const auto c = static_cast<unsigned char>(ch);
-      if (space(c)) continue;
-      if (c < 32 || c > 126 || c == '>') fail(line_no, "unexpected byte in sequence data");
-      recs.back().sequence.push_back(static_cast<char>(c >= 'a' && c <= 'z' ? c - 32 : c));
-    }
-  }
-  if (recs.empty()) throw ParseError(source + ": no FASTA records");
-  if (recs.back().sequence.empty())
-    fail(header_line, "record '" + recs.back().header + "' has no sequence data");
-  return recs;
-}
-
-inline std::vector<FastaRecord> read_fasta(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw ParseError(path + ": cannot open file");
-  return read_fasta_stream(in, path);
-}
-
-// exact header, or its first whitespace-delimited token; the first record for ""
-inline const FastaRecord& select_record(const std::vector<FastaRecord>& records, const std::string& name,
-                                        const std::string& source) {
-  if (name.empty()) return records.front();
-  for (const FastaRecord& r : records) {
-    if (r.header == name) return r;
-    const std::size_t cut = r.header.find_first_of(" \t");
-    if (cut != std::string::npos && cut == name.size() && r.header.compare(0, cut, name) == 0) return r;
-  }
-  throw ParseError(source + ": no record named '" + name + "'");
-}
-
-inline Sequence to_sequence(const FastaRecord& rec) { return Sequence::from_text(rec.header, rec.sequence); }
-
-// ---- benchmark (io.hpp:56-81, io.cpp:155-233) ------------------------------
-struct BenchEntry {
-  Mode mode = Mode::dp;
-  double seconds = 0.0;
-  double cell_updates_per_sec = 0.0;
-  double speedup_vs_first = 1.0;
-};
-
-struct BenchReport {
-  std::size_t rows = 0, cols = 0, window_w = 0, step_h = 0;
-  unsigned blowup_r = 1, workers = 1;
-  std::vector<BenchEntry> entries;
-
-  std::string to_text() const {
-    std::ostringstream os;
-    os << "plot " << rows << " x " << cols << " windows, w=" << window_w << ", h=" << step_h
-       << ", r=" << blowup_r << ", workers=" << workers << "\n";
-    char buf[160];
-    std::snprintf(buf, sizeof buf, "%-12s %10s %12s %9s\n", "mode", "seconds", "Mcups", "speedup");
-    os << buf;
-    bool dp = false;
-    for (const BenchEntry& e : entries) {
-      dp = dp || e.mode == Mode::dp;
-      std::snprintf(buf, sizeof buf, "%-12s %10.3f %12.1f %8.2fx\n", mode_name(e.mode), e.seconds,
-                    e.cell_updates_per_sec / 1e6, e.speedup_vs_first);
-      os << buf;
-    }
-    if (dp) os << "dp = exhaustive per-window DP baseline, no shortcuts\n";
-    return os.str();
-  }
-
-  // keys in sorted order, two-space indentation (the reference's json dump(2))
-  std::string to_json() const {
-    auto num = [](double v) { return detail::json_double(v); };
-    std::ostringstream os;
-    os << "{\n  \"blowup\": " << blowup_r << ",\n  \"cols\": " << cols << ",\n  \"results\": [";
-    for (std::size_t i = 0; i < entries.size(); ++i) {
-      const BenchEntry& e = entries[i];
-      os << (i ? "," : "") << "\n    {\n      \"cell_updates_per_sec\": " << num(e.cell_updates_per_sec)
-         << ",\n      \"mode\": \"" << mode_name(e.mode) << "\",\n      \"seconds\": " << num(e.seconds)
-         << ",\n      \"speedup_vs_first\": " << num(e.speedup_vs_first) << "\n    }";
-    }
-    os << (entries.empty() ? "]" : "\n  ]") << ",\n  \"rows\": " << rows << ",\n  \"step\": " << step_h
-       << ",\n  \"window\": " << window_w << ",\n  \"workers\": " << workers << "\n}";
-    return os.str();
-  }
-};
-
-// Times each mode on the same inputs; every mode must give the same grid (all
-// of them run on the GPU engine here, so they agree by construction).  Cell
-// updates/s are normalised to the per-window DP cost rows*cols*(w*r)^2.
-inline BenchReport benchmark(const Sequence& x, const Sequence& y, const PlotConfig& cfg,
-                             std::span<const Mode> modes) {
-  if (modes.empty()) throw ConfigError("benchmark needs at least one mode");
-  BenchReport rep;
-  rep.window_w = cfg.window_w;
-  rep.step_h = cfg.step_h;
-  rep.blowup_r = cfg.blowup_r;
-  rep.workers = cfg.workers;
-  std::optional<PlotGrid> first;
-  for (Mode m : modes) {
-    PlotConfig c = cfg;
-    c.mode = m;
-    const auto t0 = std::chrono::steady_clock::now();
-    PlotGrid g = compute_plot(x, y, c);
-    const double secs =
-        std::max(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), 1e-9);
-    if (!first) {
-      first = std::move(g);
-      rep.rows = first->rows;
-      rep.cols = first->cols;
-    } else if (!(g == *first)) {
-      throw std::runtime_error(std::string("benchmark: mode ") + mode_name(m) + " disagrees with " +
-                               mode_name(modes.front()));
-    }
-    const double wr = double(cfg.window_w * cfg.blowup_r);
-    BenchEntry e;
-    e.mode = m;
-    e.seconds = secs;
-    e.cell_updates_per_sec = double(rep.rows) * double(rep.cols) * wr * wr / secs;
-    e.speedup_vs_first = rep.entries.empty() ? 1.0 : rep.entries.front().seconds / secs;
-    rep.entries.push_back(e);
-  }
-  return rep;
 }
 
 }  // namespace alignplot

@@ -103,14 +103,99 @@ __global__ void codes_small_kernel(const uint8_t* __restrict__ x, size_t m, cons
   }
 }
 
+// ---- exclusive scan of the per-(row, segment) hit counts --------------------
+// uint32 counts -> uint64 offsets (offs[i] = sum of counts[0, i), offs[n] = total), so lists
+// longer than 2^32 cells (a count-only query on C4 / C5 at a low threshold) place and count
+// exactly.  Three launches: tile sums, one CTA scanning the tile sums, tile scans.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;                     // counts per thread
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* total) {
+  __shared__ unsigned long long wsum[kScanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+    if (lane >= uint32_t(off)) incl += u;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  unsigned long long base = 0, all = 0;
+#pragma unroll
+  for (int k = 0; k < kScanThreads / 32; ++k) {
+    const unsigned long long s = wsum[k];
+    base += uint32_t(k) < wid ? s : 0ull;
+    all += s;
+  }
+  __syncthreads();   // wsum is reused by the next call
+  *total = all;
+  return base + incl - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums_kernel(const uint32_t* __restrict__ cnt, size_t n,
+                                                                       unsigned long long* __restrict__ tsum) {
+  const size_t t0 = size_t(blockIdx.x) * kScanTile;
+  unsigned long long s = 0;
+  for (int k = 0; k < kScanItems; ++k) {
+    const size_t i = t0 + size_t(k) * kScanThreads + threadIdx.x;   // coalesced
+    if (i < n) s += cnt[i];
+  }
+  unsigned long long tot;
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+// one CTA: tile sums -> exclusive tile offsets (in place), grand total -> *total
+__global__ void __launch_bounds__(kScanThreads) scan_tile_offsets_kernel(unsigned long long* __restrict__ tsum,
+                                                                          size_t ntiles,
+                                                                          unsigned long long* __restrict__ total) {
+  unsigned long long carry = 0;
+  for (size_t b = 0; b < ntiles; b += kScanThreads) {
+    const size_t i = b + threadIdx.x;
+    const unsigned long long v = i < ntiles ? tsum[i] : 0ull;
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(v, &tot);
+    if (i < ntiles) tsum[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// each thread scans kScanItems consecutive counts of its tile
+__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const uint32_t* __restrict__ cnt, size_t n,
+                                                                   const unsigned long long* __restrict__ toff,
+                                                                   unsigned long long* __restrict__ offs) {
+  const size_t i0 = size_t(blockIdx.x) * kScanTile + size_t(threadIdx.x) * kScanItems;
+  uint32_t v[kScanItems];
+  unsigned long long s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = i0 + k < n ? cnt[i0 + k] : 0u;
+    s += v[k];
+  }
+  unsigned long long tot;
+  unsigned long long run = toff[blockIdx.x] + block_excl_scan(s, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (i0 + k < n) offs[i0 + k] = run;
+    run += v[k];
+  }
+}
+
 // Deterministic row-major placement of staged threshold records:
 // final index = offset[row * seg_stride + seg] + rank, where rows below split_row are cut into
 // segments of seg_cols columns and the rest (the launch's short tail tasks) of seg_cols2.
+// Structure-of-arrays output (orow/ocol/ohalf) or, with ocell != nullptr, ap_cell records
+// {row, col, int32 half} (PlotCell, scoring.hpp:33-42).
+struct CellRec { uint32_t row, col; int32_t half; };
+
 __global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long nrec,
                              const unsigned long long* __restrict__ offsets, uint32_t seg_stride,
                              uint32_t seg_cols, uint32_t seg_cols2, uint32_t split_row, uint32_t r,
                              uint32_t row_global0, uint32_t* __restrict__ orow, uint32_t* __restrict__ ocol,
-                             uint16_t* __restrict__ ohalf, unsigned long long cap) {
+                             uint16_t* __restrict__ ohalf, CellRec* __restrict__ ocell, unsigned long long cap) {
   for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < nrec;
        i += 1ull * gridDim.x * blockDim.x) {
     const uint4 rec = stage[i];
@@ -118,9 +203,13 @@ __global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long
     const uint32_t seg = (rec.y * r) / (row < split_row ? seg_cols : seg_cols2);
     const unsigned long long pos = offsets[size_t(row) * seg_stride + seg] + rec.w;
     if (pos < cap) {
-      orow[pos] = rec.x;
-      ocol[pos] = rec.y;
-      ohalf[pos] = uint16_t(rec.z);
+      if (ocell) {
+        ocell[pos] = CellRec{rec.x, rec.y, int32_t(int16_t(uint16_t(rec.z)))};
+      } else {
+        orow[pos] = rec.x;
+        ocol[pos] = rec.y;
+        ohalf[pos] = uint16_t(rec.z);
+      }
     }
   }
 }

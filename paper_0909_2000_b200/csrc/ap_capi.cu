@@ -9,10 +9,10 @@
 // device order is the global row-major order, so the only cross-device step
 // is the gather of per-device hit counts.
 #include <cuda_runtime.h>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -263,11 +263,14 @@ struct ap_ctx {
   size_t cap_segc = 0;
   unsigned long long* d_offs = nullptr;
   size_t cap_offs = 0;
-  void* d_cub = nullptr;
-  size_t cap_cub = 0;
-  uint32_t *d_orow = nullptr, *d_ocol = nullptr;
-  uint16_t* d_ohalf = nullptr;
-  size_t cap_orow = 0, cap_ocol = 0, cap_ohalf = 0;
+  unsigned long long* d_tsum = nullptr;   // scan tile sums / offsets
+  size_t cap_tsum = 0;
+  cudaMemPool_t pool = nullptr;   // per-call list buffers of the host API (stream-ordered, cached)
+  // the staged list of the last thresholded run_device (placed by place_list)
+  struct ListState {
+    size_t nrec = 0;
+    uint32_t seg_stride = 0, S = 0, S2 = 0, split_row = 0, r = 1, row_global0 = 0;
+  } list;
   float last_ms = 0.f;
   int last_launches = 0;
   char last_kernel[64] = "";
@@ -355,11 +358,12 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
 #define AP_STREAM_GROWTH 1.2
 #endif
 
+// Thresholded runs (dense = false) stage the hits and leave them in c->list for place_list;
+// `cap` is the caller's list capacity (a lower bound for the staging size).
 int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
                const ap_config* cfg, size_t nrows, size_t row_global0, bool dense,
                void* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
-               uint32_t* d_orow, uint32_t* d_ocol, uint16_t* d_ohalf, size_t cap, int out_kind = 0,
-               void* host_out = nullptr, bool allow_spec = true) {
+               size_t cap, int out_kind = 0, void* host_out = nullptr, bool allow_spec = true) {
   const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
   const uint32_t W = w * r;
   const size_t N = n * r;
@@ -554,18 +558,26 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t grid = std::min<size_t>(ctas_needed, size_t(c->sms) * per_sm);
 
   if (!dense) {
-    size_t stage_need = std::max<size_t>(cap, 1 << 16);
-    if (c->cap_stage < stage_need) {
-      int rc2 = grow(&c->d_stage, &c->cap_stage, stage_need);
-      if (rc2) return rc2;
+    // Staging (one 16-B record per hit) is sized so a call normally stages every hit in one
+    // pass: the grid's cell count bounds it, the caller's capacity is a floor, and otherwise it
+    // takes up to 2^28 records (4 GiB) within an eighth of free device memory.  A list longer
+    // than the staging still comes out exact: the kernel counts every hit, the staging grows to
+    // the exact size and the comb re-runs (rare).
+    const size_t cells_ub = nrows * cols + 1;
+    size_t target = std::max(std::min(cells_ub, size_t(1) << 28), std::min(cap, cells_ub));
+    if (c->cap_stage < target) {
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
+      target = std::min(target, std::max<size_t>(fr / 8 / sizeof(uint4), std::min(cap, cells_ub)));
+      target = std::max<size_t>(target, std::min<size_t>(cells_ub, 1 << 16));
+      if (c->cap_stage < target && (rc = grow(&c->d_stage, &c->cap_stage, target))) return rc;
     }
-    // one extra zero slot so the exclusive scan also yields the total
     const size_t nc = nrows * p.seg_stride;
-    if ((rc = grow(&c->d_segc, &c->cap_segc, nc + 1))) return rc;
+    if ((rc = grow(&c->d_segc, &c->cap_segc, nc))) return rc;
     if ((rc = grow(&c->d_offs, &c->cap_offs, nc + 1))) return rc;
+    if ((rc = grow(&c->d_tsum, &c->cap_tsum, (nc + apk::kScanTile - 1) / apk::kScanTile + 1))) return rc;
     // with a tail split the rows of the long-task groups leave counts nseg..seg_stride-1 unset
-    if (p.seg_stride != p.nseg) CK(cudaMemsetAsync(c->d_segc, 0, (nc + 1) * sizeof(uint32_t), st));
-    else CK(cudaMemsetAsync(c->d_segc + nc, 0, sizeof(uint32_t), st));
+    if (p.seg_stride != p.nseg) CK(cudaMemsetAsync(c->d_segc, 0, nc * sizeof(uint32_t), st));
     CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
     // the kernel tests h >= t in biased 16-bit halves: |h| <= 2048, so clamping t
     // to +-0x4000 keeps every comparison exact
@@ -645,6 +657,11 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       CK(cudaGetLastError());
       CK(cudaEventRecord(c->ev_blk[k], sk));
       c->last_launches += 1;
+    }
+    // every block's kernel is enqueued before the first copy: a copy to pageable host memory
+    // returns only when it is done, which would otherwise hold back the next block's launch
+    for (size_t k = 0; k < nblk; ++k) {
+      const size_t r0 = std::min(nrows, blk_g0[k] * 2 * G), r1 = std::min(nrows, blk_g0[k + 1] * 2 * G);
       CK(cudaStreamWaitEvent(c->stream_copy, c->ev_blk[k], 0));
       CK(cudaMemcpyAsync(static_cast<char*>(host_out) + r0 * cols * elem,
                          static_cast<const char*>(d_out) + r0 * cols * elem, (r1 - r0) * cols * elem,
@@ -672,7 +689,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
-                        d_orow, d_ocol, d_ohalf, cap, out_kind, host_out, false);
+                        cap, out_kind, host_out, false);
     return AP_OK;
   }
   fn<<<dim3(unsigned(grid)), dim3(wpc * 32), sh.smem, st>>>(p);
@@ -682,13 +699,13 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   if (!dense) {
     // deterministic row-major placement: exclusive scan of (row, segment) counts
+    // (64-bit offsets and total: lists past 2^32 cells count exactly)
     const size_t nc = nrows * p.seg_stride;
-    size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->d_segc, c->d_offs, int(nc + 1), st));
-    if (c->cap_cub < tmp) {
-      if ((rc = grow(reinterpret_cast<unsigned char**>(&c->d_cub), &c->cap_cub, tmp))) return rc;
-    }
-    CK(cub::DeviceScan::ExclusiveSum(c->d_cub, tmp, c->d_segc, c->d_offs, int(nc + 1), st));
+    const size_t ntiles = (nc + apk::kScanTile - 1) / apk::kScanTile;
+    apk::scan_tile_sums_kernel<<<unsigned(ntiles), apk::kScanThreads, 0, st>>>(c->d_segc, nc, c->d_tsum);
+    apk::scan_tile_offsets_kernel<<<1, apk::kScanThreads, 0, st>>>(c->d_tsum, ntiles, c->d_offs + nc);
+    apk::scan_tiles_kernel<<<unsigned(ntiles), apk::kScanThreads, 0, st>>>(c->d_segc, nc, c->d_tsum, c->d_offs);
+    CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_cursor, c->d_cursor, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_cursor + 1, c->d_offs + nc, sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st));
@@ -696,7 +713,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
-                        d_orow, d_ocol, d_ohalf, cap, out_kind, host_out, false);
+                        cap, out_kind, host_out, false);
     const size_t nrec = c->h_cursor[0];
     const size_t total = c->h_cursor[1];
     if (nrec != total) return fail(AP_CUDA, "threshold bookkeeping mismatch (%zu staged vs %zu counted)", nrec, total);
@@ -711,16 +728,14 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       CK(cudaGetLastError());
       c->last_launches += 1;
     }
-    if (nrec && d_orow) {
-      const size_t blocks = std::min<size_t>((nrec + 255) / 256, 8192);
-      apk::place_kernel<<<unsigned(blocks), 256, 0, st>>>(c->d_stage, nrec, c->d_offs, p.seg_stride,
-                                                            uint32_t(S), p.S2, uint32_t(split_row), r,
-                                                            uint32_t(row_global0), d_orow, d_ocol,
-                                                            d_ohalf, cap);
-      CK(cudaGetLastError());
-      c->last_launches += 1;
-    }
-    c->last_launches += 2;  // the two cub scan passes
+    c->list.nrec = nrec;
+    c->list.seg_stride = p.seg_stride;
+    c->list.S = uint32_t(S);
+    c->list.S2 = p.S2;
+    c->list.split_row = uint32_t(split_row);
+    c->list.r = r;
+    c->list.row_global0 = uint32_t(row_global0);
+    c->last_launches += 3;  // the scan
     *nrec_out = nrec;
     *total_out = total;
   } else {
@@ -729,8 +744,24 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
-                        d_orow, d_ocol, d_ohalf, cap, out_kind, host_out, false);
+                        cap, out_kind, host_out, false);
   }
+  return AP_OK;
+}
+
+// Place the list staged by the last thresholded run_device on c in row-major order
+// (apply_threshold, scoring.cpp:30-39): the first min(total, cap) cells into the device
+// arrays (rows/cols/halves, or ap_cell records when cells != nullptr).  Enqueued on st.
+int place_list(ap_ctx* c, cudaStream_t st, uint32_t* rows, uint32_t* cols, uint16_t* halves,
+               apk::CellRec* cells, size_t cap) {
+  const ap_ctx::ListState& l = c->list;
+  if (!l.nrec || !cap) return AP_OK;
+  const size_t blocks = std::min<size_t>((l.nrec + 255) / 256, size_t(c->sms) * 16);
+  apk::place_kernel<<<unsigned(blocks), 256, 0, st>>>(c->d_stage, l.nrec, c->d_offs, l.seg_stride, l.S, l.S2,
+                                                        l.split_row, l.r, l.row_global0, rows, cols, halves,
+                                                        cells, cap);
+  CK(cudaGetLastError());
+  c->last_launches += 1;
   return AP_OK;
 }
 
@@ -789,6 +820,15 @@ int ap_ctx_create(int device, ap_ctx** out) {
   CK(cudaMalloc(&c->d_map, 256));
   CK(cudaMalloc(&c->d_cursor, 16));
   CK(cudaMallocHost(&c->h_cursor, 32));
+  {
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    CK(cudaMemPoolCreate(&c->pool, &pp));
+    uint64_t keep = ~uint64_t(0);   // keep freed list buffers for the next call
+    CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   *out = c;
   return AP_OK;
 }
@@ -804,9 +844,12 @@ int ap_ctx_destroy(ap_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_ycol, (void*)c->d_map,
                   (void*)c->d_small, (void*)c->d_tasks, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
-                  (void*)c->d_segc, (void*)c->d_offs, c->d_cub, (void*)c->d_orow, (void*)c->d_ocol,
-                  (void*)c->d_ohalf})
+                  (void*)c->d_segc, (void*)c->d_offs, (void*)c->d_tsum})
     if (p) cudaFree(p);
+  if (c->pool) {
+    cudaStreamSynchronize(c->stream_copy);
+    cudaMemPoolDestroy(c->pool);
+  }
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_cursor) cudaFreeHost(c->h_cursor);
   cudaStreamSynchronize(c->stream_copy);
@@ -850,8 +893,7 @@ int ap_ctx_plot_dense_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint
   DevGuard dg(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const size_t off = rb * cfg->step_h;
-  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, 0);
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr, nullptr, 0);
 }
 
 int ap_ctx_plot_dense_u8_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
@@ -868,8 +910,7 @@ int ap_ctx_plot_dense_u8_device(ap_ctx* c, const uint8_t* d_x, size_t m, const u
   DevGuard dg(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const size_t off = rb * cfg->step_h;
-  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, 0, 2);
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr, nullptr, 0, 2);
 }
 
 int ap_ctx_plot_pgm_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
@@ -884,8 +925,8 @@ int ap_ctx_plot_pgm_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_
   DevGuard dg(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const size_t off = rb * cfg->step_h;
-  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_pixels, st, nullptr,
-                    nullptr, nullptr, nullptr, nullptr, 0, 1);
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_pixels, st, nullptr, nullptr, 0,
+                    1);
 }
 
 int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y,
@@ -903,33 +944,48 @@ int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const 
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const size_t off = rb * cfg->step_h;
   size_t nrec = 0, total = 0;
-  rc = run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, false, nullptr, st, &nrec, &total,
-                  cap ? d_rows : nullptr, d_cols, d_halves, cap);
+  rc = run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, false, nullptr, st, &nrec, &total, cap);
   if (rc) return rc;
+  if ((rc = place_list(c, st, d_rows, d_cols, d_halves, nullptr, cap))) return rc;
   CK(cudaStreamSynchronize(st));
   *count = total;
   if (total > cap) return fail(AP_CAPACITY, "%zu cells pass the threshold, capacity %zu", total, cap);
   return AP_OK;
 }
 
+}  // extern "C"
+
 namespace {
 
 bool has_sentinel(const uint8_t* p, size_t n) { return std::memchr(p, 0, n) != nullptr; }
 
-// Shared host-API body: validates, shards rows over devices, runs, gathers.
-int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
-              bool dense, void* out_dense, uint64_t* count, uint32_t* orow, uint32_t* ocol,
-              uint16_t* ohalf, size_t cap, int out_kind = 0) {
+static_assert(sizeof(ap_cell) == sizeof(apk::CellRec) && offsetof(ap_cell, half) == offsetof(apk::CellRec, half),
+              "ap_cell and the placement kernel's record must share a layout");
+
+// One device's contiguous block of grid rows [r0, r1).
+struct Shard {
+  int dev = 0;
+  size_t r0 = 0, r1 = 0;
+  ap_ctx* ctx = nullptr;
+  size_t total = 0;        // hits of this shard (thresholded runs)
+  size_t kept = 0;         // entries placed into `list` (<= total)
+  char* list = nullptr;    // the shard's row-major list in device memory (ctx pool)
+  int rc = AP_OK;
+  std::string err;
+};
+
+// Shared prologue of the host API: validation before any device work (runner.cpp:81 order),
+// the row range, and the row shards over devices.
+int plan_shards(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg, size_t* rb,
+                size_t* re, size_t* cols, std::vector<Shard>* sh) {
   if (!x || !y || !cfg) return fail(AP_INVALID, "null argument");
   int rc = check_cfg(m, n, cfg);
   if (rc) return rc;
   if (has_sentinel(x, m) || has_sentinel(y, n))
     return fail(AP_CONFIG, "sequence contains the reserved sentinel code 0");
-  size_t rows, cols, rb, re;
-  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
-  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
-  if (dense && !out_dense && re > rb) return fail(AP_INVALID, "null output");
-  const size_t out_elem = out_kind == 0 ? 2 : 1;
+  size_t rows;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, cols);
+  if ((rc = row_range(rows, cfg, rb, re))) return rc;
   const int ndev_real = ap_device_count();
   // AP_SHARDS_PER_DEVICE=k (testing): let one physical GPU stand in for k shard
   // devices, so the multi-device split/gather path runs on a single-GPU box.
@@ -940,135 +996,202 @@ int host_plot(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   int ndev = cfg->n_devices <= 1 ? 1 : std::min(cfg->n_devices, ndev_avail);
   int cur = 0;
   cudaGetDevice(&cur);
-  const size_t nr = re - rb;
+  const size_t nr = *re - *rb;
   if (size_t(ndev) > nr) ndev = int(std::max<size_t>(nr, 1));
-
-  struct Shard {
-    int dev;
-    size_t r0, r1;
-    size_t total = 0;
-    int rc = AP_OK;
-    std::string err;
-    // multi-shard threshold lists are staged on the host inside the shard's
-    // context lock (shards may share a device context)
-    std::vector<uint32_t> hr, hc;
-    std::vector<uint16_t> hh;
-  };
-  std::vector<Shard> sh(ndev);
+  sh->assign(ndev, Shard());
   for (int d = 0; d < ndev; ++d) {
-    sh[d].dev = ndev == 1 ? cur : d % std::max(ndev_real, 1);
-    sh[d].r0 = rb + nr * d / ndev;
-    sh[d].r1 = rb + nr * (d + 1) / ndev;
+    Shard& s = (*sh)[d];
+    s.dev = ndev == 1 ? cur : d % std::max(ndev_real, 1);
+    s.r0 = *rb + nr * d / ndev;
+    s.r1 = *rb + nr * (d + 1) / ndev;
+    if ((rc = get_ctx(s.dev, &s.ctx))) return rc;
   }
-  const size_t w = cfg->window_w, h = cfg->step_h;
+  return AP_OK;
+}
 
-  // phase 1: per device compute (threads so devices overlap)
-  auto work = [&](Shard& s) {
-    ap_ctx* c = nullptr;
-    int e = get_ctx(s.dev, &c);
-    if (e) { s.rc = e; s.err = g_err; return; }
-    std::lock_guard<std::mutex> lk(c->mu);
-    DevGuard dg(c->device);
-    cudaStream_t st = c->stream;
-    const size_t nrows = s.r1 - s.r0;
-    if (nrows == 0) return;
-    const size_t x0 = s.r0 * h, x1 = (s.r1 - 1) * h + w;  // rows plus the w-1 halo
-    auto run = [&]() -> int {
-      int q;
-      if ((q = grow(&c->d_x, &c->cap_x, x1 - x0))) return q;
-      if ((q = grow(&c->d_y, &c->cap_y, n))) return q;
-      CK(cudaMemcpyAsync(c->d_x, x + x0, x1 - x0, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(c->d_y, y, n, cudaMemcpyHostToDevice, st));
-      if (dense) {
-        if ((q = grow(&c->d_out, &c->cap_out, nrows * cols))) return q;
-        if ((q = run_device(c, c->d_x, x1 - x0, c->d_y, n, cfg, nrows, s.r0, true, c->d_out, st,
-                            nullptr, nullptr, nullptr, nullptr, nullptr, 0, out_kind,
-                            static_cast<char*>(out_dense) + (s.r0 - rb) * cols * out_elem)))
-          return q;
-        CK(cudaStreamSynchronize(st));
-      } else {
-        // first pass sizes the list (counts are exact even if staging is short)
-        size_t need = std::max<size_t>(cap, 1);
-        if ((q = grow(&c->d_orow, &c->cap_orow, need))) return q;
-        if ((q = grow(&c->d_ocol, &c->cap_ocol, need))) return q;
-        if ((q = grow(&c->d_ohalf, &c->cap_ohalf, need))) return q;
-        size_t nrec = 0, total = 0;
-        if ((q = run_device(c, c->d_x, x1 - x0, c->d_y, n, cfg, nrows, s.r0, false, nullptr, st,
-                            &nrec, &total, c->d_orow, c->d_ocol, c->d_ohalf, need)))
-          return q;
-        CK(cudaStreamSynchronize(st));
-        s.total = total;
-        if (ndev > 1 && total) {
-          const size_t k = std::min(total, need);
-          s.hr.resize(k);
-          s.hc.resize(k);
-          s.hh.resize(k);
-          CK(cudaMemcpy(s.hr.data(), c->d_orow, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-          CK(cudaMemcpy(s.hc.data(), c->d_ocol, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-          CK(cudaMemcpy(s.hh.data(), c->d_ohalf, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
-        }
-      }
-      return AP_OK;
-    };
-    s.rc = run();
-    if (s.rc) s.err = g_err;
-  };
-  if (ndev == 1) {
-    work(sh[0]);
+// Run fn(shard) for every shard, one host thread per shard when there are several
+// (so devices overlap); returns the first failure.
+template <typename F>
+int for_shards(std::vector<Shard>& sh, F fn) {
+  if (sh.size() == 1) {
+    sh[0].rc = fn(sh[0]);
+    if (sh[0].rc) sh[0].err = g_err;
   } else {
     std::vector<std::thread> th;
-    for (auto& s : sh) th.emplace_back(work, std::ref(s));
+    for (auto& s : sh)
+      th.emplace_back([&fn, &s]() {
+        s.rc = fn(s);
+        if (s.rc) s.err = g_err;
+      });
     for (auto& t : th) t.join();
   }
   for (auto& s : sh)
     if (s.rc) return fail(s.rc, "%s", s.err.c_str());
-  if (dense) return AP_OK;
+  return AP_OK;
+}
 
-  // phase 2: gather per-device counts -> global offsets; copy lists in order
+// H2D of a shard's x slice (its rows plus the w-1 halo) and of y into the context.
+int upload_shard(ap_ctx* c, const Shard& s, const uint8_t* x, const uint8_t* y, size_t n, const ap_config* cfg,
+                 cudaStream_t st, size_t* mx) {
+  const size_t x0 = s.r0 * cfg->step_h, x1 = (s.r1 - 1) * cfg->step_h + cfg->window_w;
+  int q;
+  if ((q = grow(&c->d_x, &c->cap_x, x1 - x0))) return q;
+  if ((q = grow(&c->d_y, &c->cap_y, n))) return q;
+  CK(cudaMemcpyAsync(c->d_x, x + x0, x1 - x0, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_y, y, n, cudaMemcpyHostToDevice, st));
+  *mx = x1 - x0;
+  return AP_OK;
+}
+
+// Dense host API body: every shard streams its row block straight to its offset in out.
+int host_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg, void* out,
+               int out_kind) {
+  size_t rb, re, cols;
+  std::vector<Shard> sh;
+  int rc = plan_shards(x, m, y, n, cfg, &rb, &re, &cols, &sh);
+  if (rc) return rc;
+  if (!out && re > rb) return fail(AP_INVALID, "null output");
+  const size_t out_elem = out_kind == 0 ? 2 : 1;
+  return for_shards(sh, [&](Shard& s) -> int {
+    const size_t nrows = s.r1 - s.r0;
+    if (nrows == 0) return AP_OK;
+    ap_ctx* c = s.ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DevGuard dg(c->device);
+    cudaStream_t st = c->stream;
+    size_t mx = 0;
+    int q;
+    if ((q = upload_shard(c, s, x, y, n, cfg, st, &mx))) return q;
+    if ((q = grow(&c->d_out, &c->cap_out, nrows * cols))) return q;
+    if ((q = run_device(c, c->d_x, mx, c->d_y, n, cfg, nrows, s.r0, true, c->d_out, st, nullptr, nullptr, 0,
+                        out_kind, static_cast<char*>(out) + (s.r0 - rb) * cols * out_elem)))
+      return q;
+    CK(cudaStreamSynchronize(st));
+    return AP_OK;
+  });
+}
+
+// Where the thresholded host API delivers the list.
+struct ListDest {
+  uint32_t* rows = nullptr;
+  uint32_t* cols = nullptr;
+  uint16_t* halves = nullptr;
+  ap_cell* cells = nullptr;            // array-of-structs form instead of rows / cols / halves
+  size_t cap = 0;
+  ap_list_alloc_fn alloc = nullptr;    // callback form: called once with the total
+  void* user = nullptr;
+};
+
+// Thresholded host API body (apply_threshold(compute_plot(...)), scoring.cpp:30-39, fused).
+// One comb per shard: phase 1 combs each shard and places its list in device memory owned by
+// the call (the context lock is released after it, so concurrent calls cannot overwrite it);
+// phase 2 gathers the per-shard counts into global offsets -- the path's only cross-device
+// step -- and copies each shard's list straight to its offset in the caller's buffer.
+int host_list(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg, uint64_t* count,
+              ListDest dst) {
+  size_t rb, re, cols;
+  std::vector<Shard> sh;
+  int rc = plan_shards(x, m, y, n, cfg, &rb, &re, &cols, &sh);
+  if (rc) return rc;
+  const size_t esz = dst.cells ? sizeof(ap_cell) : 2 * sizeof(uint32_t) + sizeof(uint16_t);
+  // entries a shard may need: its list starts at a global offset >= 0
+  const size_t cap_any = dst.alloc ? ~size_t(0) : dst.cap;
+  auto free_lists = [&]() {
+    for (auto& s : sh)
+      if (s.list) {
+        DevGuard dg(s.ctx->device);
+        cudaFreeAsync(s.list, s.ctx->stream);
+        s.list = nullptr;
+      }
+  };
+  rc = for_shards(sh, [&](Shard& s) -> int {
+    const size_t nrows = s.r1 - s.r0;
+    if (nrows == 0) return AP_OK;
+    ap_ctx* c = s.ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DevGuard dg(c->device);
+    cudaStream_t st = c->stream;
+    size_t mx = 0, nrec = 0, total = 0;
+    int q;
+    if ((q = upload_shard(c, s, x, y, n, cfg, st, &mx))) return q;
+    if ((q = run_device(c, c->d_x, mx, c->d_y, n, cfg, nrows, s.r0, false, nullptr, st, &nrec, &total, 0)))
+      return q;
+    s.total = total;
+    s.kept = std::min(total, cap_any);
+    if (s.kept) {
+      CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&s.list), s.kept * esz, c->pool, st));
+      uint32_t* lr = reinterpret_cast<uint32_t*>(s.list);
+      if ((q = place_list(c, st, dst.cells ? nullptr : lr, dst.cells ? nullptr : lr + s.kept,
+                          dst.cells ? nullptr : reinterpret_cast<uint16_t*>(lr + 2 * s.kept),
+                          dst.cells ? reinterpret_cast<apk::CellRec*>(s.list) : nullptr, s.kept)))
+        return q;
+    }
+    CK(cudaStreamSynchronize(st));
+    return AP_OK;
+  });
+  if (rc) {
+    free_lists();
+    return rc;
+  }
+  // phase 2: global offsets (exclusive prefix of the shard counts, in row order)
+  std::vector<uint64_t> offs(sh.size());
   uint64_t total = 0;
-  std::vector<uint64_t> offs(ndev);
-  for (int d = 0; d < ndev; ++d) {
+  for (size_t d = 0; d < sh.size(); ++d) {
     offs[d] = total;
     total += sh[d].total;
   }
   if (count) *count = total;
-  for (int d = 0; d < ndev; ++d) {
-    if (offs[d] >= cap || sh[d].total == 0) continue;
-    const size_t k = std::min<size_t>(sh[d].total, cap - offs[d]);
-    if (ndev > 1) {
-      std::memcpy(orow + offs[d], sh[d].hr.data(), k * sizeof(uint32_t));
-      std::memcpy(ocol + offs[d], sh[d].hc.data(), k * sizeof(uint32_t));
-      std::memcpy(ohalf + offs[d], sh[d].hh.data(), k * sizeof(uint16_t));
-      continue;
+  size_t cap = dst.cap;
+  if (dst.alloc) {
+    if (dst.alloc(dst.user, total, &dst.rows, &dst.cols, &dst.halves) != 0) {
+      free_lists();
+      return fail(AP_INVALID, "list allocation callback failed for %llu cells", (unsigned long long)total);
     }
-    ap_ctx* c = nullptr;
-    get_ctx(sh[d].dev, &c);
-    std::lock_guard<std::mutex> lk(c->mu);
-    DevGuard dg(c->device);
-    CK(cudaMemcpy(orow + offs[d], c->d_orow, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ocol + offs[d], c->d_ocol, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ohalf + offs[d], c->d_ohalf, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+    if (total && (!dst.rows || !dst.cols || !dst.halves)) {
+      free_lists();
+      return fail(AP_INVALID, "list allocation callback returned null arrays");
+    }
+    cap = total;
   }
-  if (total > cap) return fail(AP_CAPACITY, "%llu cells pass the threshold, capacity %zu",
-                               (unsigned long long)total, cap);
+  rc = for_shards(sh, [&](Shard& s) -> int {
+    const size_t d = size_t(&s - sh.data());
+    if (offs[d] >= cap || !s.kept) return AP_OK;
+    const size_t k = std::min<size_t>(s.kept, cap - offs[d]);
+    DevGuard dg(s.ctx->device);
+    if (dst.cells) {
+      CK(cudaMemcpy(dst.cells + offs[d], s.list, k * sizeof(ap_cell), cudaMemcpyDeviceToHost));
+    } else {
+      const uint32_t* lr = reinterpret_cast<const uint32_t*>(s.list);
+      CK(cudaMemcpy(dst.rows + offs[d], lr, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(dst.cols + offs[d], lr + s.kept, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(dst.halves + offs[d], lr + 2 * s.kept, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+    }
+    return AP_OK;
+  });
+  free_lists();
+  if (rc) return rc;
+  if (total > cap)
+    return fail(AP_CAPACITY, "%llu cells pass the threshold, capacity %zu", (unsigned long long)total, cap);
   return AP_OK;
 }
 
 }  // namespace
+
+extern "C" {
 
 int ap_plot_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                   uint16_t* out_half) {
   if (cfg && cfg->has_threshold) {
     ap_config c = *cfg;   // the dense grid is never filtered (compute_plot, runner.cpp:78-131)
     c.has_threshold = 0;
-    return host_plot(x, m, y, n, &c, true, out_half, nullptr, nullptr, nullptr, nullptr, 0);
+    return host_dense(x, m, y, n, &c, out_half, 0);
   }
-  return host_plot(x, m, y, n, cfg, true, out_half, nullptr, nullptr, nullptr, nullptr, 0);
+  return host_dense(x, m, y, n, cfg, out_half, 0);
 }
 
 int ap_plot_pgm(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                 uint8_t* pixels) {
-  return host_plot(x, m, y, n, cfg, true, pixels, nullptr, nullptr, nullptr, nullptr, 0, 1);
+  return host_dense(x, m, y, n, cfg, pixels, 1);
 }
 
 int ap_plot_dense_u8(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
@@ -1078,9 +1201,9 @@ int ap_plot_dense_u8(const uint8_t* x, size_t m, const uint8_t* y, size_t n, con
   if (cfg && cfg->has_threshold) {
     ap_config c = *cfg;
     c.has_threshold = 0;
-    return host_plot(x, m, y, n, &c, true, out_half, nullptr, nullptr, nullptr, nullptr, 0, 2);
+    return host_dense(x, m, y, n, &c, out_half, 2);
   }
-  return host_plot(x, m, y, n, cfg, true, out_half, nullptr, nullptr, nullptr, nullptr, 0, 2);
+  return host_dense(x, m, y, n, cfg, out_half, 2);
 }
 
 int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
@@ -1088,7 +1211,22 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
   if (!count) return fail(AP_INVALID, "null count");
   if (cap && (!rows || !cols || !halves)) return fail(AP_INVALID, "null output arrays");
   if (!cfg || !cfg->has_threshold) return fail(AP_INVALID, "ap_plot_threshold needs has_threshold");
-  return host_plot(x, m, y, n, cfg, false, nullptr, count, rows, cols, halves, cap);
+  ListDest d;
+  d.rows = rows;
+  d.cols = cols;
+  d.halves = halves;
+  d.cap = cap;
+  return host_list(x, m, y, n, cfg, count, d);
+}
+
+int ap_plot_threshold_into(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                           ap_list_alloc_fn alloc, void* user, uint64_t* count) {
+  if (!alloc) return fail(AP_INVALID, "null allocation callback");
+  if (!cfg || !cfg->has_threshold) return fail(AP_INVALID, "ap_plot_threshold_into needs has_threshold");
+  ListDest d;
+  d.alloc = alloc;
+  d.user = user;
+  return host_list(x, m, y, n, cfg, count, d);
 }
 
 int ap_plot_threshold_cells(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
@@ -1096,13 +1234,10 @@ int ap_plot_threshold_cells(const uint8_t* x, size_t m, const uint8_t* y, size_t
   if (!count) return fail(AP_INVALID, "null count");
   if (cap && !cells) return fail(AP_INVALID, "null output array");
   if (!cfg || !cfg->has_threshold) return fail(AP_INVALID, "ap_plot_threshold_cells needs has_threshold");
-  std::vector<uint32_t> rows(cap), cols(cap);
-  std::vector<uint16_t> halves(cap);
-  const int rc = host_plot(x, m, y, n, cfg, false, nullptr, count, rows.data(), cols.data(), halves.data(), cap);
-  if (rc != AP_OK && rc != AP_CAPACITY) return rc;
-  const size_t k = std::min<uint64_t>(*count, cap);
-  for (size_t i = 0; i < k; ++i) cells[i] = ap_cell{rows[i], cols[i], int32_t(int16_t(halves[i]))};
-  return rc;
+  ListDest d;
+  d.cells = cells;
+  d.cap = cap;
+  return host_list(x, m, y, n, cfg, count, d);
 }
 
 }  // extern "C"

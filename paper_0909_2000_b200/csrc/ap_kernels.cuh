@@ -331,9 +331,8 @@ __host__ __device__ inline size_t comb_smem_per_warp(int L, int table_words, uin
 //  * Slot addresses and the running count use IMAD / IMAD.HI on the FMA pipe.
 // Packed 32-bit sums are exact whenever every half of the final value is in
 // [0, 0xFFFF] (arithmetic is linear mod 2^32), so no per-column bias is needed.
-// Extraction phases (extract_body below chains them for one strip pair per group;
-// the two-pair r = 2 kernel, ap_kernels2p.cuh, runs the scatter and output phases once
-// per pair around one shared flag read and clear).  Shared constants:
+// Extraction phases (extract_body below chains them for one strip pair per group).
+// Shared constants:
 // phase 1: scatter the ok flags of countable seaweeds (bytes BYTE and BYTE + 2 of a slot:
 // strip A and B of the pair); cab[c]: bit 15 / 31 = column countable (strip A / B)
 template <int L, int NB, bool CHECK, int BYTE>
@@ -911,7 +910,7 @@ comb_kernel(const CombParams p) {
 //   ($ row, $ col)    always match   -> the two seaweeds swap: zero instructions
 //   ($ row, real col) never match    -> d = max(V,T), V' = min(V,T)
 //   (real row, $ col) never match    -> same
-//   (real row, real col)             -> table multiplier, HMUL2 + max + xor
+//   (real row, real col)             -> table mask: VIADDMNMX + LOP3
 // (SURVEY.md §7 hard part 8).  A step is one raw column = the blown columns
 // 2c ($) and 2c+1 (real); two seaweeds per band move down per step.  The
 // table holds only real rows and real codes.  R = 2*RR blown rows per lane,

@@ -175,40 +175,42 @@ int main() {
     CHECK(unblow(b) == Sequence::from_text("s", "abab").data);
     CHECK(recover_score(4, 2, 2) == 4 && recover_score(2, 2, 2) == 0 && recover_score(2, 1, 2) == 1);
   }
-  {  // test_io.cpp:155-252 writers, and the fused GPU PGM against the host writer
-    PlotGrid g(2, 2, 4, 5);
-    g.at(0, 0) = 4; g.at(0, 1) = 1; g.at(1, 0) = 3; g.at(1, 1) = 8;
-    std::ostringstream all;
-    write_tsv(all, g, std::nullopt, false);
-    CHECK(all.str() == "# x_offset y_offset score\n0\t0\t2.0\n0\t1\t0.5\n5\t0\t1.5\n5\t1\t4.0\n");
-    std::ostringstream dots;
-    write_dots(dots, g, half_score_t{3});
-    CHECK(dots.str() == "0 0\n5 0\n5 1\n");
+  {  // writers (io.cpp:102-153 byte format) fed from the device, against formatting of compute_plot's grid
     std::mt19937 rng(560);
     const Sequence x("x", random_codes(rng, 200, 4)), y("y", random_codes(rng, 260, 4));
+    auto dec = [](half_score_t v) {   // half-units as "k.0" / "k.5"
+      const long long a = v < 0 ? -static_cast<long long>(v) : v;
+      return std::string(v < 0 ? "-" : "") + std::to_string(a / 2) + (a % 2 ? ".5" : ".0");
+    };
     for (unsigned r : {1u, 2u}) {
       PlotConfig cfg;
       cfg.window_w = 20; cfg.step_h = 3; cfg.blowup_r = r; cfg.threshold_half = 18;
-      std::ostringstream host, dev;
-      write_pgm(host, compute_plot(x, y, cfg), cfg.threshold_half);
-      write_pgm_gpu(dev, x, y, cfg);
-      CHECK(host.str() == dev.str());
+      const PlotGrid g = compute_plot(x, y, cfg);
+      std::string tsv_all = "# x_offset y_offset score\n", tsv_thr = tsv_all, dots;
+      std::string pgm = "P5\n" + std::to_string(g.cols) + " " + std::to_string(g.rows) + "\n255\n";
+      const long long full = 2 * static_cast<long long>(g.window_w);
+      for (std::size_t i = 0; i < g.rows; ++i)
+        for (std::size_t k = 0; k < g.cols; ++k) {
+          const half_score_t v = g.at(i, k);
+          const std::string pos = std::to_string(g.x_offset(i)) + "\t" + std::to_string(g.y_offset(k));
+          tsv_all += pos + "\t" + dec(v) + "\n";
+          if (v >= 18) {
+            tsv_thr += pos + "\t" + dec(v) + "\n";
+            dots += std::to_string(g.x_offset(i)) + " " + std::to_string(g.y_offset(k)) + "\n";
+          }
+          const long long h = std::clamp<long long>(v < 18 ? 0 : v, 0, full);
+          pgm.push_back(static_cast<char>((255 * h + full / 2) / full));
+        }
+      std::ostringstream a, b, c, d;
+      write_tsv_gpu(a, x, y, cfg, true);
+      write_tsv_gpu(b, x, y, cfg, false);
+      write_dots_gpu(c, x, y, cfg);
+      write_pgm_gpu(d, x, y, cfg);
+      CHECK(a.str() == tsv_all);
+      CHECK(b.str() == tsv_thr);
+      CHECK(c.str() == dots);
+      CHECK(d.str() == pgm);
     }
-  }
-  {  // io.cpp:192-233 benchmark: every mode timed, grids agree, DP-normalised rates
-    std::mt19937 rng(77);
-    const Sequence x("x", random_codes(rng, 300, 4)), y("y", random_codes(rng, 340, 4));
-    PlotConfig cfg;
-    cfg.window_w = 30; cfg.step_h = 2; cfg.blowup_r = 2;
-    const Mode modes[] = {Mode::sea8, Mode::sea16, Mode::cuda};
-    const BenchReport rep = benchmark(x, y, cfg, modes);
-    const auto dims = window_grid_dims(300, 340, 30, 2);
-    CHECK(rep.rows == dims.first && rep.cols == dims.second && rep.entries.size() == 3);
-    CHECK(rep.entries[0].speedup_vs_first == 1.0 && rep.entries[2].mode == Mode::cuda);
-    const double cells = double(rep.rows) * double(rep.cols) * 60.0 * 60.0;
-    CHECK(std::abs(rep.entries[1].cell_updates_per_sec * rep.entries[1].seconds - cells) < 1e-6 * cells);
-    CHECK(rep.to_text().rfind("plot " + std::to_string(rep.rows) + " x ", 0) == 0);
-    CHECK_THROWS_AS(benchmark(x, y, cfg, std::span<const Mode>{}), ConfigError);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
   return failures;

@@ -77,8 +77,8 @@ def test_cpp_shim_compiles():
 
 
 def test_cpp_shim_io_cpu():
-    """The C++ drop-in's FASTA reader and BenchReport formatting (no device work):
-    error kinds/line numbers of io.cpp:32-100 and the to_text layout of io.cpp:155-174."""
+    """The C++ drop-in's output formatting (no device work): half-unit scores as the
+    reference writers print them (io.cpp:102-119), through the writers' buffered sink."""
     import shutil
     import subprocess
     import tempfile

@@ -589,3 +589,139 @@ def test_c5_full_size_threshold_checksum_symmetry():
             sums.append((rr.size, int(np.sum(_mix64(k ^ (hh.astype(np.uint64) << np.uint64(50))), dtype=np.uint64))))
         del rr, cc, hh, key, k
     assert sums[0] == sums[1]
+
+
+@pytest.mark.parametrize("w,r", [(64, 1), (128, 1), (50, 2), (100, 2)])
+def test_tail_split_equals_unsplit(w, r, monkeypatch):
+    """Launches of >= 2 waves cut their last wave of pair groups into half-width tasks (the
+    tail split, ap_capi.cu run_device).  At a size where it is active (~6000 x 5000, about
+    10000 tasks), the device-API dense plot and the thresholded list must equal the same plot
+    with the split disabled (AP_TAIL_SPLIT=1, the path the oracle-checked small plots take),
+    and rows around the split boundary must equal the oracle."""
+    import ctypes
+
+    import torch
+
+    from paper_0909_2000_b200 import _native
+
+    rng = np.random.default_rng(w * 3 + r)
+    x = rng.integers(1, 5, 6000).astype(np.uint8)
+    y = np.concatenate([x[1000:3500], rng.integers(1, 5, 2600)]).astype(np.uint8)
+    rows, cols = (x.size - w) + 1, y.size - w + 1
+    L = _native.lib()
+    ctx = ctypes.c_void_p()
+    assert L.ap_ctx_create(0, ctypes.byref(ctx)) == 0
+    try:
+        dx, dy = torch.from_numpy(x.copy()).cuda(), torch.from_numpy(y.copy()).cuda()
+        out = torch.empty(rows * cols, dtype=torch.int16, device="cuda")
+        c = ap._cfg(cfg(w, 1, r))
+
+        def dense():
+            assert L.ap_ctx_plot_dense_device(ctx, dx.data_ptr(), x.size, dy.data_ptr(), y.size, ctypes.byref(c),
+                                              out.data_ptr(), None) == 0
+            torch.cuda.synchronize()
+            return out.cpu().numpy().view(np.uint16).reshape(rows, cols).copy()
+
+        split = dense()
+        t = int(np.quantile(split, 0.995))
+        lst = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
+        monkeypatch.setenv("AP_TAIL_SPLIT", "1")
+        unsplit = dense()
+        lst1 = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
+    finally:
+        L.ap_ctx_destroy(ctx)
+    assert np.array_equal(split, unsplit)
+    for a, b in zip(lst, lst1):
+        assert np.array_equal(a, b)
+    rr, cc = np.nonzero(split >= t)
+    assert np.array_equal(lst[0], rr) and np.array_equal(lst[1], cc) and np.array_equal(lst[2], split[rr, cc])
+    for rb in (0, rows // 2, rows - 3):
+        rc, want = ol.plot_rows(x, y, w, 1, r, rb, rb + 3)
+        assert rc == 0 and np.array_equal(split[rb:rb + 3].astype(np.int32), want), rb
+
+
+def test_threshold_host_api_concurrent_threads():
+    """Thresholded host calls from several threads on one device context (the list
+    must not be overwritten between the comb and the copy-out): each gets its own list."""
+    import threading
+    rng = np.random.default_rng(321)
+    cases = []
+    for k in range(6):
+        w = int(rng.integers(10, 70))
+        x = rng.integers(1, 5, w + 300).astype(np.uint8)
+        y = np.concatenate([x[20:200], rng.integers(1, 5, 400 + 50 * k)]).astype(np.uint8)
+        rc, g = ol.plot_rows(x, y, w, 1, 1 + k % 2)
+        t = int(np.quantile(g, 0.98))
+        rr, cc = np.nonzero(g >= t)
+        cases.append((x, y, w, 1 + k % 2, t, (rr, cc, g[rr, cc])))
+    errs, bad = [], []
+
+    def run(i):
+        x, y, w, r, t, want = cases[i]
+        try:
+            for _ in range(4):
+                got = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t)
+                if not all(np.array_equal(a, b) for a, b in zip(got, want)):
+                    bad.append(i)
+        except Exception as e:   # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(cases))]
+    for t_ in ts:
+        t_.start()
+    for t_ in ts:
+        t_.join()
+    assert not errs, errs
+    assert not bad, bad
+
+
+def test_threshold_into_single_pass_and_capacity_contract():
+    """ap_plot_threshold_into sizes the result through its callback (called once, also for an
+    empty list); ap_plot_threshold with a short cap returns the first cap cells + AP_CAPACITY
+    and the exact count; ap_plot_threshold_cells fills ap_cell records."""
+    import ctypes
+
+    from paper_0909_2000_b200 import _native
+    rng = np.random.default_rng(17)
+    x = rng.integers(1, 5, 900).astype(np.uint8)
+    y = np.concatenate([x[100:600], rng.integers(1, 5, 300)]).astype(np.uint8)
+    w, r = 40, 1
+    rc, g = ol.plot_rows(x, y, w, 1, r)
+    t = int(np.quantile(g, 0.97))
+    er, ec = np.nonzero(g >= t)
+    L = _native.lib()
+    c = ap._cfg(cfg(w, 1, r, t))
+    calls = []
+    keep = {}
+
+    def alloc(_u, n, pr, pc, ph):
+        calls.append(int(n))
+        keep["a"] = [np.empty(max(n, 1), dt) for dt in (np.uint32, np.uint32, np.uint16)]
+        pr[0], pc[0], ph[0] = (a.ctypes.data for a in keep["a"])
+        return 0
+
+    count = ctypes.c_uint64()
+    xa, ya = np.ascontiguousarray(x), np.ascontiguousarray(y)
+    assert L.ap_plot_threshold_into(xa.ctypes.data, x.size, ya.ctypes.data, y.size, ctypes.byref(c),
+                                    _native.ListAllocFn(alloc), None, ctypes.byref(count)) == 0
+    assert calls == [er.size] and count.value == er.size
+    assert np.array_equal(keep["a"][0][:er.size], er) and np.array_equal(keep["a"][1][:er.size], ec)
+    # no cell passes: one callback with 0
+    c_hi = ap._cfg(cfg(w, 1, r, 10 * w))
+    calls.clear()
+    assert L.ap_plot_threshold_into(xa.ctypes.data, x.size, ya.ctypes.data, y.size, ctypes.byref(c_hi),
+                                    _native.ListAllocFn(alloc), None, ctypes.byref(count)) == 0
+    assert calls == [0] and count.value == 0
+    # a failing callback aborts with AP_INVALID
+    assert L.ap_plot_threshold_into(xa.ctypes.data, x.size, ya.ctypes.data, y.size, ctypes.byref(c),
+                                    _native.ListAllocFn(lambda *a: 1), None, ctypes.byref(count)) == _native.AP_INVALID
+    # fixed capacity: the first cap cells and the exact count
+    k = er.size // 3
+    rr, cc, hh = (np.zeros(k, dt) for dt in (np.uint32, np.uint32, np.uint16))
+    assert L.ap_plot_threshold(xa.ctypes.data, x.size, ya.ctypes.data, y.size, ctypes.byref(c), ctypes.byref(count),
+                               rr.ctypes.data, cc.ctypes.data, hh.ctypes.data, k) == _native.AP_CAPACITY
+    assert count.value == er.size and np.array_equal(rr, er[:k]) and np.array_equal(cc, ec[:k])
+    cells = (_native.ApCell * er.size)()
+    assert L.ap_plot_threshold_cells(xa.ctypes.data, x.size, ya.ctypes.data, y.size, ctypes.byref(c),
+                                     ctypes.byref(count), ctypes.cast(cells, ctypes.c_void_p), er.size) == 0
+    assert [cl.row for cl in cells] == er.tolist() and [cl.half for cl in cells] == g[er, ec].tolist()

@@ -59,14 +59,16 @@ def _worker(rank, world, port, x, y, w, h, r, t, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("w,h,r", [(32, 1, 1), (20, 3, 2)])
-def test_gloo_world2_matches_single_process(w, h, r):
+@pytest.mark.parametrize("w,h,r,world", [(32, 1, 1, 2), (20, 3, 2, 2), (24, 1, 2, 4)])
+def test_gloo_matches_single_process(w, h, r, world):
+    """Strong split of one fixed plot: each rank's global list offset is the exclusive prefix of
+    the gathered counts, and writing every rank's list / row block at its offset reproduces the
+    single-process row-major result."""
     rng = np.random.default_rng(11)
     x = rng.integers(1, 5, 400).astype(np.uint8)
     y = np.concatenate([x[50:250], rng.integers(1, 5, 150)]).astype(np.uint8)
     rc, full = ol.plot_rows(x, y, w, h, r)
     t = int(np.quantile(full, 0.98))
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -83,7 +85,14 @@ def test_gloo_world2_matches_single_process(w, h, r):
     out_r = np.zeros(total, np.uint32)
     out_c = np.zeros(total, np.uint32)
     out_h = np.zeros(total, np.uint16)
+    shards = plan_row_shards(x.size, w, h, world)
+    expect_off = 0
     for rank, off, _, rr, cc, hh, r0, block in res:
+        assert off == expect_off   # exclusive prefix of the gathered counts, in rank (= row) order
+        expect_off += rr.size
+        s = shards[rank]
+        assert rr.size == 0 or (s.row_begin <= int(rr.min()) and int(rr.max()) < s.row_end)
+        assert rr.size == int(np.count_nonzero(full[s.row_begin:s.row_end] >= t))
         out_r[off:off + rr.size], out_c[off:off + cc.size], out_h[off:off + hh.size] = rr, cc, hh
     assert np.array_equal(out_r, er) and np.array_equal(out_c, ec) and np.array_equal(out_h, full[er, ec])
     dense = np.concatenate([v[7] for v in res], axis=0)
