@@ -62,9 +62,12 @@ typedef struct ap_config {
 /* window_grid_dims (model.cpp:63-72): rows = (m-w)/h + 1, cols = n-w+1. */
 int ap_grid_dims(size_t m, size_t n, size_t w, size_t h, size_t* rows, size_t* cols);
 
-/* PlotConfig::validate (model.cpp:46-61) plus the engine's own limit
- * (w*r <= AP_MAX_BLOWN_WINDOW). */
-#define AP_MAX_BLOWN_WINDOW 1024
+/* PlotConfig::validate (model.cpp:46-61) with the sea16 lane bound: blown windows
+ * w*r <= AP_MAX_BLOWN_WINDOW (model.cpp:57-59).  Windows up to AP_PACKED_WINDOW run on
+ * the packed 16-bit-key kernels; larger ones on the large-window path (32-bit keys,
+ * one CTA per strip). */
+#define AP_MAX_BLOWN_WINDOW 65534
+#define AP_PACKED_WINDOW 1024
 int ap_validate(size_t m, size_t n, const ap_config* cfg);
 
 /* Dense plot of grid rows [row_begin, row_end): out_half receives

@@ -17,7 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AP_LIB_PATH") or os.path.join(_HERE, "libalignplot_b200.so")
 
 AP_OK, AP_CONFIG, AP_EMPTY, AP_INVALID, AP_CUDA, AP_NODEV, AP_CAPACITY, AP_NOMEM = range(8)
-AP_MAX_BLOWN_WINDOW = 1024
+AP_MAX_BLOWN_WINDOW = 65534   # sea16 bound (model.cpp:57-59)
+AP_PACKED_WINDOW = 1024       # larger blown windows take the large-window kernels
 
 # Every symbol declared in include/alignplot_b200.h (checked by tests/test_abi.py).
 EXPORTS = (

@@ -24,8 +24,8 @@ Every reference ``Mode`` is served by the CUDA engine: the reference proves
 all engines produce the identical grid (acceptance.cpp:34-73), so routing
 them to one engine preserves outputs, while ``PlotConfig.validate`` keeps each
 mode's own limits (sea8 w <= 254, sea16 w*r <= 65534) so a config the
-reference rejects is still rejected.  ``Mode.cuda`` carries only the engine's
-limit (w*r <= 1024).
+reference rejects is still rejected.  ``Mode.cuda`` carries the sea16 bound
+(w*r <= 65534); blown windows above 1024 run on the large-window kernels.
 """
 from __future__ import annotations
 
@@ -149,7 +149,7 @@ class PlotConfig:
             raise ConfigError("sea16 mode supports blown windows up to 65534")
         window_grid_dims(m, n, self.window_w, self.step_h)
         if self.window_w * self.blowup_r > _native.AP_MAX_BLOWN_WINDOW:
-            raise ConfigError(f"CUDA engine supports blown windows up to {_native.AP_MAX_BLOWN_WINDOW} "
+            raise ConfigError(f"blown windows up to {_native.AP_MAX_BLOWN_WINDOW} are supported "
                               f"(got {self.window_w * self.blowup_r})")
 
 

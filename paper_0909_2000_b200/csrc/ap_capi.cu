@@ -25,6 +25,7 @@
 #include "../../include/alignplot_b200.h"
 #include "ap_aux_kernels.cuh"
 #include "ap_kernels.cuh"
+#include "ap_wide_kernels.cuh"
 
 namespace {
 
@@ -265,6 +266,10 @@ struct ap_ctx {
   size_t cap_offs = 0;
   unsigned long long* d_tsum = nullptr;   // scan tile sums / offsets
   size_t cap_tsum = 0;
+  int32_t* d_wkeys = nullptr;   // large-window path: per-strip start keys
+  size_t cap_wkeys = 0;
+  uint8_t* d_wok = nullptr;     // large-window path: per-strip extraction flags
+  size_t cap_wok = 0;
   cudaMemPool_t pool = nullptr;   // per-call list buffers of the host API (stream-ordered, cached)
   // the staged list of the last thresholded run_device (placed by place_list)
   struct ListState {
@@ -335,7 +340,7 @@ int check_cfg(size_t m, size_t n, const ap_config* cfg) {
     return fail(AP_EMPTY, "no window of size %zu fits inputs of lengths %zu and %zu",
                 size_t(cfg->window_w), m, n);
   if (cfg->window_w * cfg->blowup_r > AP_MAX_BLOWN_WINDOW)
-    return fail(AP_CONFIG, "CUDA engine supports blown windows up to %d (got %zu)",
+    return fail(AP_CONFIG, "blown windows up to %d are supported (sea16 bound, model.cpp:57-59; got %zu)",
                 AP_MAX_BLOWN_WINDOW, size_t(cfg->window_w * cfg->blowup_r));
   if (n * cfg->blowup_r > 0x7FFFFFF0ull) return fail(AP_CONFIG, "y too long for the CUDA engine");
   return AP_OK;
@@ -347,6 +352,142 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
   *re = cfg->row_end ? std::min<size_t>(cfg->row_end, rows) : rows;
   if (*rb > *re) return fail(AP_INVALID, "row_begin > row_end");
   if (*re - *rb > 0xFFFFFFF0ull) return fail(AP_INVALID, "too many rows in one call");
+  return AP_OK;
+}
+
+// Thresholded runs: size the staging and the per-(row, segment) count buffers, zero the cursor.
+// Staging (one 16-B record per hit) is sized so a call normally stages every hit in one
+// pass: the grid's cell count bounds it, the caller's capacity is a floor, and otherwise it
+// takes up to 2^28 records (4 GiB) within an eighth of free device memory.  A list longer
+// than the staging still comes out exact: the kernel counts every hit, the staging grows to
+// the exact size and the comb re-runs (rare).
+int stage_prepare(ap_ctx* c, size_t nrows, size_t cols, size_t cap, size_t seg_stride, bool zero_counts,
+                  cudaStream_t st) {
+  int rc;
+  const size_t cells_ub = nrows * cols + 1;
+  size_t target = std::max(std::min(cells_ub, size_t(1) << 28), std::min(cap, cells_ub));
+  if (c->cap_stage < target) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
+    target = std::min(target, std::max<size_t>(fr / 8 / sizeof(uint4), std::min(cap, cells_ub)));
+    target = std::max<size_t>(target, std::min<size_t>(cells_ub, 1 << 16));
+    if (c->cap_stage < target && (rc = grow(&c->d_stage, &c->cap_stage, target))) return rc;
+  }
+  const size_t nc = nrows * seg_stride;
+  if ((rc = grow(&c->d_segc, &c->cap_segc, nc))) return rc;
+  if ((rc = grow(&c->d_offs, &c->cap_offs, nc + 1))) return rc;
+  if ((rc = grow(&c->d_tsum, &c->cap_tsum, (nc + apk::kScanTile - 1) / apk::kScanTile + 1))) return rc;
+  if (zero_counts) CK(cudaMemsetAsync(c->d_segc, 0, nc * sizeof(uint32_t), st));
+  CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
+  return AP_OK;
+}
+
+// Exclusive scan of the nc per-(row, segment) hit counts into 64-bit offsets (the total at
+// offs[nc]), then the staged-record cursor and the total to the host (h_cursor[0], [1]).
+int scan_counts(ap_ctx* c, size_t nc, cudaStream_t st) {
+  const size_t ntiles = (nc + apk::kScanTile - 1) / apk::kScanTile;
+  apk::scan_tile_sums_kernel<<<unsigned(ntiles), apk::kScanThreads, 0, st>>>(c->d_segc, nc, c->d_tsum);
+  apk::scan_tile_offsets_kernel<<<1, apk::kScanThreads, 0, st>>>(c->d_tsum, ntiles, c->d_offs + nc);
+  apk::scan_tiles_kernel<<<unsigned(ntiles), apk::kScanThreads, 0, st>>>(c->d_segc, nc, c->d_tsum, c->d_offs);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->h_cursor, c->d_cursor, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_cursor + 1, c->d_offs + nc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  c->last_launches += 3;
+  return AP_OK;
+}
+
+// The large-window path (W = w*r > AP_PACKED_WINDOW, up to 65534; ap_wide_kernels.cuh): one
+// CTA per strip combs it band by band with exact 32-bit keys, then one CTA per strip
+// extracts its row.  Strips run in batches bounded by the key scratch (~2 GiB).  Code
+// streams are already built (x codes, the $-interleaved y stream, $ code `sent`).
+int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, bool dense, void* d_out,
+             cudaStream_t st, size_t* nrec_out, size_t* total_out, size_t cap, int out_kind, void* host_out,
+             uint32_t sent, size_t n) {
+  const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
+  const uint32_t W = w * r;
+  const size_t N = n * r;
+  const size_t cols = n - w + 1;
+  int rc;
+  const uint32_t warps = std::min<uint32_t>(apk::kWideMaxWarps, (W + 32 * apk::kWideRows - 1) / (32 * apk::kWideRows));
+  const uint32_t band_rows = warps * 32 * apk::kWideRows;
+  apk::WideParams p{};
+  p.xcode = c->d_xcode;
+  p.ycode = c->d_ycode;
+  p.h = h;
+  p.w = w;
+  p.r = r;
+  p.W = W;
+  p.N = uint32_t(N);
+  p.sent_code = sent;
+  p.band_rows = band_rows;
+  p.bands = (W + band_rows - 1) / band_rows;
+  p.cols = uint32_t(cols);
+  p.row_global0 = uint32_t(row_global0);
+  p.out = static_cast<uint16_t*>(d_out);
+  p.out8 = static_cast<uint8_t*>(d_out);
+  p.out_kind = uint32_t(out_kind);
+  p.pgm_threshold = cfg->threshold_half;
+  p.has_pgm_threshold = cfg->has_threshold ? 1u : 0u;
+  p.dense = dense ? 1u : 0u;
+  if (!dense) {
+    if ((rc = stage_prepare(c, nrows, cols, cap, 1, false, st))) return rc;
+    p.t_half = cfg->threshold_half;
+    p.stage = c->d_stage;
+    p.cursor = c->d_cursor;
+    p.stage_cap = c->cap_stage;
+    p.seg_counts = c->d_segc;
+  }
+  const size_t batch = std::max<size_t>(1, std::min<size_t>(nrows, (size_t(2) << 30) / (5 * N)));
+  if ((rc = grow(&c->d_wkeys, &c->cap_wkeys, batch * N))) return rc;
+  if ((rc = grow(&c->d_wok, &c->cap_wok, batch * N))) return rc;
+  p.keys = c->d_wkeys;
+  p.ok = c->d_wok;
+  CK(cudaEventRecord(c->ev0, st));
+  auto launch_all = [&]() -> int {
+    for (size_t r0 = 0; r0 < nrows; r0 += batch) {
+      apk::WideParams q = p;
+      q.strips = uint32_t(std::min(batch, nrows - r0));
+      q.row0 = uint32_t(r0);
+      q.xcode = c->d_xcode + r0 * h;
+      apk::wide_comb_kernel<<<q.strips, warps * 32, 0, st>>>(q);
+      CK(cudaGetLastError());
+      apk::wide_extract_kernel<<<q.strips, apk::kWideExtThreads, 0, st>>>(q);
+      CK(cudaGetLastError());
+      c->last_launches += 2;
+    }
+    return AP_OK;
+  };
+  if ((rc = launch_all())) return rc;
+  CK(cudaEventRecord(c->ev1, st));
+  std::snprintf(c->last_kernel, sizeof(c->last_kernel), "combw<%u,%d>", warps, apk::kWideRows);
+  if (dense) {
+    if (host_out) {
+      const size_t elem = out_kind == 0 ? 2 : 1;
+      CK(cudaMemcpyAsync(host_out, d_out, nrows * cols * elem, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return AP_OK;
+  }
+  if ((rc = scan_counts(c, nrows, st))) return rc;
+  CK(cudaStreamSynchronize(st));
+  const size_t nrec = c->h_cursor[0], total = c->h_cursor[1];
+  if (nrec != total) return fail(AP_CUDA, "threshold bookkeeping mismatch (%zu staged vs %zu counted)", nrec, total);
+  if (nrec > c->cap_stage) {   // staging overflowed: grow to the exact size and recompute (rare)
+    if ((rc = grow(&c->d_stage, &c->cap_stage, nrec))) return rc;
+    p.stage = c->d_stage;
+    p.stage_cap = c->cap_stage;
+    CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
+    if ((rc = launch_all())) return rc;
+  }
+  c->list.nrec = nrec;
+  c->list.seg_stride = 1;
+  c->list.S = uint32_t(N + 1);   // one segment per row
+  c->list.S2 = uint32_t(N + 1);
+  c->list.split_row = uint32_t(nrows);
+  c->list.r = r;
+  c->list.row_global0 = uint32_t(row_global0);
+  *nrec_out = nrec;
+  *total_out = total;
   return AP_OK;
 }
 
@@ -385,7 +526,9 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const bool overrides = std::getenv("AP_SHAPE") || std::getenv("AP_SHAPE2") || std::getenv("AP_NO_R2");
   const uint64_t skey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(out_kind) << 2) | (dense ? 1 : 0);
   const auto spec_hit = c->last_sigma.find(skey);
-  const bool speculate = allow_spec && !overrides && !std::getenv("AP_NO_SPEC") && spec_hit != c->last_sigma.end();
+  const bool wide = W > AP_PACKED_WINDOW;   // the large-window path plans nothing by sigma
+  const bool speculate = !wide && allow_spec && !overrides && !std::getenv("AP_NO_SPEC") &&
+                         spec_hit != c->last_sigma.end();
   // small inputs take the fused single-CTA code-stream kernel (one launch) when speculating
   const bool fused_codes = speculate && mx + N <= (size_t(1) << 20);
   uint32_t sigma_y;
@@ -415,6 +558,19 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   };
   const uint32_t sent = sigma_y;
   const uint32_t sigma = sigma_y + (r == 2 ? 1 : 0);
+  if (wide) {
+    int q;
+    const size_t ytot = (N + 256 + 31) / 32 * 32;
+    if ((q = grow(&c->d_xcode, &c->cap_xcode, mx))) return q;
+    if ((q = grow(&c->d_ycode, &c->cap_ycode, ytot))) return q;
+    apk::xcode_kernel<<<std::min<size_t>((mx + 255) / 256, 4096), 256, 0, st>>>(d_x, mx, c->d_map, c->d_xcode);
+    apk::ycode_kernel<<<std::min<size_t>((ytot + 255) / 256, 4096), 256, 0, st>>>(d_y, n, r, sent, c->d_map,
+                                                                                  c->d_ycode, ytot, nullptr);
+    CK(cudaGetLastError());
+    c->last_launches += 3;
+    return run_wide(c, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out, cap, out_kind, host_out,
+                    sent, n);
+  }
 
   // launch plan (shape choice, function attributes, occupancy), cached per context;
   // tuning overrides (AP_SHAPE, AP_SHAPE2, AP_NO_R2) bypass the cache
@@ -558,27 +714,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t grid = std::min<size_t>(ctas_needed, size_t(c->sms) * per_sm);
 
   if (!dense) {
-    // Staging (one 16-B record per hit) is sized so a call normally stages every hit in one
-    // pass: the grid's cell count bounds it, the caller's capacity is a floor, and otherwise it
-    // takes up to 2^28 records (4 GiB) within an eighth of free device memory.  A list longer
-    // than the staging still comes out exact: the kernel counts every hit, the staging grows to
-    // the exact size and the comb re-runs (rare).
-    const size_t cells_ub = nrows * cols + 1;
-    size_t target = std::max(std::min(cells_ub, size_t(1) << 28), std::min(cap, cells_ub));
-    if (c->cap_stage < target) {
-      size_t fr = 0, tot = 0;
-      if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
-      target = std::min(target, std::max<size_t>(fr / 8 / sizeof(uint4), std::min(cap, cells_ub)));
-      target = std::max<size_t>(target, std::min<size_t>(cells_ub, 1 << 16));
-      if (c->cap_stage < target && (rc = grow(&c->d_stage, &c->cap_stage, target))) return rc;
-    }
-    const size_t nc = nrows * p.seg_stride;
-    if ((rc = grow(&c->d_segc, &c->cap_segc, nc))) return rc;
-    if ((rc = grow(&c->d_offs, &c->cap_offs, nc + 1))) return rc;
-    if ((rc = grow(&c->d_tsum, &c->cap_tsum, (nc + apk::kScanTile - 1) / apk::kScanTile + 1))) return rc;
     // with a tail split the rows of the long-task groups leave counts nseg..seg_stride-1 unset
-    if (p.seg_stride != p.nseg) CK(cudaMemsetAsync(c->d_segc, 0, nc * sizeof(uint32_t), st));
-    CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
+    if ((rc = stage_prepare(c, nrows, cols, cap, p.seg_stride, p.seg_stride != p.nseg, st))) return rc;
     // the kernel tests h >= t in biased 16-bit halves: |h| <= 2048, so clamping t
     // to +-0x4000 keeps every comparison exact
     p.t_half = std::min<int32_t>(0x4000, std::max<int32_t>(-0x4000, cfg->threshold_half));
@@ -700,15 +837,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   if (!dense) {
     // deterministic row-major placement: exclusive scan of (row, segment) counts
     // (64-bit offsets and total: lists past 2^32 cells count exactly)
-    const size_t nc = nrows * p.seg_stride;
-    const size_t ntiles = (nc + apk::kScanTile - 1) / apk::kScanTile;
-    apk::scan_tile_sums_kernel<<<unsigned(ntiles), apk::kScanThreads, 0, st>>>(c->d_segc, nc, c->d_tsum);
-    apk::scan_tile_offsets_kernel<<<1, apk::kScanThreads, 0, st>>>(c->d_tsum, ntiles, c->d_offs + nc);
-    apk::scan_tiles_kernel<<<unsigned(ntiles), apk::kScanThreads, 0, st>>>(c->d_segc, nc, c->d_tsum, c->d_offs);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(c->h_cursor, c->d_cursor, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(c->h_cursor + 1, c->d_offs + nc, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
+    if ((rc = scan_counts(c, nrows * p.seg_stride, st))) return rc;
     if (speculate) CK(cudaMemcpyAsync(c->h_small, c->d_small, 12, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
@@ -735,7 +864,6 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     c->list.split_row = uint32_t(split_row);
     c->list.r = r;
     c->list.row_global0 = uint32_t(row_global0);
-    c->last_launches += 3;  // the scan
     *nrec_out = nrec;
     *total_out = total;
   } else {
@@ -844,7 +972,7 @@ int ap_ctx_destroy(ap_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_ycol, (void*)c->d_map,
                   (void*)c->d_small, (void*)c->d_tasks, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
-                  (void*)c->d_segc, (void*)c->d_offs, (void*)c->d_tsum})
+                  (void*)c->d_segc, (void*)c->d_offs, (void*)c->d_tsum, (void*)c->d_wkeys, (void*)c->d_wok})
     if (p) cudaFree(p);
   if (c->pool) {
     cudaStreamSynchronize(c->stream_copy);

@@ -59,8 +59,11 @@ def test_validate_host_only():
     assert v(200, 200, 100, 0, 2) == _native.AP_CONFIG
     assert v(200, 200, 100, 5, 3) == _native.AP_CONFIG
     assert v(50, 200, 100, 5, 2) == _native.AP_EMPTY
-    assert v(2000, 2000, 513, 1, 2) == _native.AP_CONFIG  # engine limit: w*r <= 1024
-    assert v(2000, 2000, 512, 1, 2) == 0
+    # the sea16 lane bound (model.cpp:57-59): w*r <= 65534, above 1024 on the large-window path
+    assert v(2000, 2000, 513, 1, 2) == 0
+    assert v(70000, 70000, 65534, 1, 1) == 0 and v(70000, 70000, 32767, 1, 2) == 0
+    assert v(70000, 70000, 65535, 1, 1) == _native.AP_CONFIG
+    assert v(70000, 70000, 32768, 1, 2) == _native.AP_CONFIG
 
 
 def test_cpp_shim_compiles():

@@ -725,3 +725,48 @@ def test_threshold_into_single_pass_and_capacity_contract():
     assert L.ap_plot_threshold_cells(xa.ctypes.data, x.size, ya.ctypes.data, y.size, ctypes.byref(c),
                                      ctypes.byref(count), ctypes.cast(cells, ctypes.c_void_p), er.size) == 0
     assert [cl.row for cl in cells] == er.tolist() and [cl.half for cl in cells] == g[er, ec].tolist()
+
+
+@pytest.mark.parametrize("w,r,h", [(1025, 1, 1), (513, 2, 1), (4096, 1, 2), (2048, 2, 1), (20000, 1, 1),
+                                   (10000, 2, 3), (65534, 1, 1), (32767, 2, 1)])
+def test_large_windows_vs_reference(w, r, h):
+    """Blown windows above the packed kernels' 1024 run on the large-window path (32-bit keys,
+    one CTA per strip, band by band); the reference's sea16 engine plots any w*r <= 65534
+    (model.cpp:57-59, lane_kernel.cpp:117-123).  Dense grids and thresholded lists against
+    oracle/_ref sea16 at w*r = 1025, 1026, 4096, 20000 and the 65534 bound."""
+    import os
+    assert ol.ref_available()
+    rng = np.random.default_rng(w * 2 + r + h)
+    W = w * r
+    rows = 5 if W <= 20000 else 2
+    m = w + (rows - 1) * h
+    x = rng.integers(1, 5, m).astype(np.uint8)
+    blk = x[: w].copy()
+    flip = rng.random(blk.size) < 0.15
+    blk[flip] = rng.integers(1, 5, int(flip.sum()))
+    y = np.concatenate([rng.integers(1, 5, 120), blk, rng.integers(1, 5, 180)]).astype(np.uint8)
+    rc, want, err = ol.ref_compute_plot(x, y, w, h, r, ol.SEA16, os.cpu_count() or 8)
+    assert rc == 0, err
+    got = gpu_grid(x, y, w, h, r)
+    assert got.shape == want.shape and np.array_equal(got, want), (w, r, h)
+    t = int(np.quantile(want, 0.9))
+    rr, cc = np.nonzero(want >= t)
+    gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)
+    assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
+
+
+def test_large_window_many_rows_and_bound():
+    """Large-window path over many rows (several strips per launch, both modes, row ranges)
+    against the oracle, and the sea16 bound: w*r = 65535 is a ConfigError before device work."""
+    rng = np.random.default_rng(1100)
+    for w, r in ((1100, 1), (600, 2)):
+        x = rng.integers(1, 5, w + 300).astype(np.uint8)
+        y = np.concatenate([x[100:w + 200], rng.integers(1, 5, 400)]).astype(np.uint8)
+        rc, want = ol.plot_rows(x, y, w, 1, r, 40, 140)
+        assert rc == 0
+        got = gpu_grid(x, y, w, 1, r, 40, 140)
+        assert np.array_equal(got, want), (w, r)
+    with pytest.raises(ap.ConfigError):
+        ap.plot_dense_u16(np.ones(70000, np.uint8), np.ones(70000, np.uint8), cfg(65535, 1, 1))
+    with pytest.raises(ap.ConfigError):
+        ap.plot_dense_u16(np.ones(40000, np.uint8), np.ones(40000, np.uint8), cfg(32768, 1, 2))
