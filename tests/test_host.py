@@ -46,8 +46,11 @@ def test_config_validation_matches_reference_order():
         s8.validate(300, 300)
     ap.PlotConfig(window_w=254, step_h=1, blowup_r=1, mode=ap.Mode.sea8).validate(300, 300)
     ap.PlotConfig(window_w=255, step_h=1, blowup_r=1, mode=ap.Mode.sea16).validate(300, 300)
-    with pytest.raises(ap.ConfigError):   # the CUDA engine's own limit
-        ap.PlotConfig(window_w=513, step_h=1, blowup_r=2, mode=ap.Mode.cuda).validate(2000, 2000)
+    # Mode.cuda: the sea16 bound (model.cpp:57-59), w*r <= 65534
+    ap.PlotConfig(window_w=513, step_h=1, blowup_r=2, mode=ap.Mode.cuda).validate(2000, 2000)
+    ap.PlotConfig(window_w=32767, step_h=1, blowup_r=2, mode=ap.Mode.cuda).validate(40000, 40000)
+    with pytest.raises(ap.ConfigError):
+        ap.PlotConfig(window_w=32768, step_h=1, blowup_r=2, mode=ap.Mode.cuda).validate(40000, 40000)
 
 
 def test_plan_strips():
