@@ -90,9 +90,10 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
  * scoring.cpp:30-39): the plot is combed once; when the total is known the
  * engine calls alloc(user, count, &rows, &cols, &halves) exactly once (also for
  * count 0) to get host arrays of at least `count` entries, then writes the
- * row-major list into them.  A nonzero return from alloc aborts with AP_INVALID. */
+ * row-major list into them (int32 scores: every window size).  A nonzero return
+ * from alloc aborts with AP_INVALID. */
 typedef int (*ap_list_alloc_fn)(void* user, uint64_t count, uint32_t** rows, uint32_t** cols,
-                                uint16_t** halves);
+                                int32_t** halves);
 int ap_plot_threshold_into(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                            ap_list_alloc_fn alloc, void* user, uint64_t* count);
 
@@ -115,6 +116,12 @@ int ap_plot_threshold_cells(const uint8_t* x, size_t m, const uint8_t* y, size_t
  * device-to-host bytes of the uint16 layout. */
 int ap_plot_dense_u8(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                      uint8_t* out_half);
+
+/* As ap_plot_dense with int32 half-units -- PlotGrid::values' own type (model.hpp:95-114).
+ * Every config: the uint16 entry points return AP_CONFIG for LCS plots with w > 32767,
+ * whose scores (up to 2w half-units) exceed 16 bits. */
+int ap_plot_dense_i32(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                      int32_t* out_half);
 
 /* Dense 8-bit PGM raster of rows [row_begin, row_end), the pixels of
  * write_pgm (io.cpp:136-153) quantised inside the comb kernel:
@@ -150,6 +157,10 @@ int ap_ctx_plot_dense_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const ui
 /* As ap_plot_dense_u8 on device pointers (stream semantics of ap_ctx_plot_dense_device). */
 int ap_ctx_plot_dense_u8_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
                                 const ap_config* cfg, uint8_t* d_out, void* stream);
+
+/* As ap_plot_dense_i32 on device pointers (stream semantics of ap_ctx_plot_dense_device). */
+int ap_ctx_plot_dense_i32_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                                 const ap_config* cfg, int32_t* d_out, void* stream);
 
 /* As ap_plot_pgm on device pointers (stream semantics of ap_ctx_plot_dense_device). */
 int ap_ctx_plot_pgm_device(ap_ctx* ctx, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,

@@ -23,7 +23,7 @@ AP_PACKED_WINDOW = 1024       # larger blown windows take the large-window kerne
 # Every symbol declared in include/alignplot_b200.h (checked by tests/test_abi.py).
 EXPORTS = (
     "ap_grid_dims", "ap_validate", "ap_plot_dense", "ap_plot_dense_u8", "ap_plot_threshold", "ap_plot_pgm",
-    "ap_plot_threshold_cells", "ap_plot_threshold_into",
+    "ap_plot_threshold_cells", "ap_plot_threshold_into", "ap_plot_dense_i32", "ap_ctx_plot_dense_i32_device",
     "ap_last_error",
     "ap_device_count", "ap_ctx_create", "ap_ctx_destroy", "ap_ctx_plot_dense_device",
     "ap_ctx_plot_threshold_device", "ap_ctx_plot_pgm_device", "ap_ctx_plot_dense_u8_device",
@@ -49,7 +49,7 @@ class ApConfig(ctypes.Structure):
     ]
 
 
-# int (*ap_list_alloc_fn)(void* user, uint64_t count, uint32_t** rows, uint32_t** cols, uint16_t** halves)
+# int (*ap_list_alloc_fn)(void* user, uint64_t count, uint32_t** rows, uint32_t** cols, int32_t** halves)
 ListAllocFn = ctypes.CFUNCTYPE(c_int, c_void_p, c_uint64, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p))
 
 _lib = None
@@ -81,6 +81,11 @@ def lib() -> ctypes.CDLL:
     L.ap_plot_threshold_into.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig), ListAllocFn,
                                          c_void_p, POINTER(c_uint64)]
     L.ap_plot_threshold_into.restype = c_int
+    L.ap_plot_dense_i32.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig), c_void_p]
+    L.ap_plot_dense_i32.restype = c_int
+    L.ap_ctx_plot_dense_i32_device.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t,
+                                               POINTER(ApConfig), c_void_p, c_void_p]
+    L.ap_ctx_plot_dense_i32_device.restype = c_int
     L.ap_plot_dense_u8.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t, POINTER(ApConfig), c_void_p]
     L.ap_plot_dense_u8.restype = c_int
     L.ap_ctx_plot_dense_u8_device.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t,

@@ -301,10 +301,30 @@ def plot_dense_u8(x, y, cfg: PlotConfig, row_begin: int = 0, row_end: int = 0) -
     return out
 
 
+def plot_dense_i32(x, y, cfg: PlotConfig, row_begin: int = 0, row_end: int = 0) -> np.ndarray:
+    """Dense int32 half-unit grid (PlotGrid's own type) via ap_plot_dense_i32: every window size,
+    including LCS plots with w > 32767 whose scores exceed 16 bits."""
+    xa, ya = _codes(x), _codes(y)
+    rows, cols = window_grid_dims(xa.size, ya.size, cfg.window_w, cfg.step_h)
+    re = rows if row_end == 0 else min(row_end, rows)
+    out = np.empty((max(re - row_begin, 0), cols), dtype=np.int32)
+    _raise(_native.lib().ap_plot_dense_i32(_ptr(xa), xa.size, _ptr(ya), ya.size,
+                                           ctypes.byref(_cfg(cfg, row_begin, row_end)), _ptr(out)))
+    return out
+
+
+def scores_fit_u16(cfg: PlotConfig) -> bool:
+    """Half-unit scores lie in [0, 2w]; only LCS plots with w > 32767 leave uint16."""
+    return not (cfg.blowup_r == 1 and 2 * cfg.window_w > 65535)
+
+
 def compute_plot(x: Sequence, y: Sequence, cfg: PlotConfig) -> PlotGrid:
-    """runner.cpp:78-131 on the CUDA engine: validate first, then the dense grid (int32 half-units)."""
+    """runner.cpp:78-131 on the CUDA engine: validate first, then the dense grid (int32 half-units;
+    transferred as uint16 whenever the scores fit, half the device-to-host bytes)."""
     cfg.validate(x.size(), y.size())
     rows, cols = window_grid_dims(x.size(), y.size(), cfg.window_w, cfg.step_h)
+    if not scores_fit_u16(cfg):
+        return PlotGrid(rows, cols, cfg.window_w, cfg.step_h, 0, 0, plot_dense_i32(x, y, cfg).reshape(-1))
     u16 = plot_dense_u16(x, y, cfg)
     return PlotGrid(rows, cols, cfg.window_w, cfg.step_h, 0, 0, u16.reshape(-1).astype(np.int32))
 
@@ -337,7 +357,7 @@ def plot_threshold_arrays(x, y, cfg: PlotConfig, t_half: int, cap: Optional[int]
         try:
             held["r"] = np.empty(max(int(n), 1), dtype=np.uint32)
             held["c"] = np.empty(max(int(n), 1), dtype=np.uint32)
-            held["h"] = np.empty(max(int(n), 1), dtype=np.uint16)
+            held["h"] = np.empty(max(int(n), 1), dtype=np.int32)
         except MemoryError:
             return 1
         pr[0] = held["r"].ctypes.data

@@ -215,10 +215,14 @@ inline PlotGrid compute_plot(const Sequence& x, const Sequence& y, const PlotCon
   cfg.validate(x.size(), y.size());
   const auto [rows, cols] = window_grid_dims(x.size(), y.size(), cfg.window_w, cfg.step_h);
   PlotGrid grid(rows, cols, cfg.window_w, cfg.step_h);
-  std::vector<std::uint16_t> half(rows * cols);
   PlotConfig dense = cfg;
   dense.threshold_half.reset();
   const ap_config c = dense.to_c();
+  if (cfg.blowup_r == 1 && 2 * cfg.window_w > 65535) {   // scores beyond 16 bits: straight into the grid
+    detail::check(ap_plot_dense_i32(x.data.data(), x.size(), y.data.data(), y.size(), &c, grid.values.data()));
+    return grid;
+  }
+  std::vector<std::uint16_t> half(rows * cols);   // half the device-to-host bytes, widened here
   detail::check(ap_plot_dense(x.data.data(), x.size(), y.data.data(), y.size(), &c, half.data()));
   std::copy(half.begin(), half.end(), grid.values.begin());
   return grid;
@@ -284,10 +288,10 @@ inline std::vector<PlotCell> compute_plot_threshold(const Sequence& x, const Seq
   const ap_config c = tc.to_c();
   struct Lists {
     std::vector<std::uint32_t> r, c;
-    std::vector<std::uint16_t> h;
+    std::vector<std::int32_t> h;
   } lists;
   auto alloc = [](void* user, std::uint64_t count, std::uint32_t** rows, std::uint32_t** cols,
-                  std::uint16_t** halves) -> int {
+                  std::int32_t** halves) -> int {
     auto* l = static_cast<Lists*>(user);
     l->r.resize(count);
     l->c.resize(count);
@@ -301,7 +305,7 @@ inline std::vector<PlotCell> compute_plot_threshold(const Sequence& x, const Seq
   detail::check(ap_plot_threshold_into(x.data.data(), x.size(), y.data.data(), y.size(), &c, alloc, &lists, &count));
   std::vector<PlotCell> out(count);
   for (std::size_t k = 0; k < count; ++k)
-    out[k] = {lists.r[k], lists.c[k], static_cast<half_score_t>(static_cast<std::int16_t>(lists.h[k]))};
+    out[k] = {lists.r[k], lists.c[k], lists.h[k]};
   return out;
 }
 
@@ -352,15 +356,14 @@ inline void for_dense(const Sequence& x, const Sequence& y, const PlotConfig& cf
   PlotConfig dc = cfg;
   dc.threshold_half.reset();
   const std::size_t block = std::max<std::size_t>(1, (std::size_t(32) << 20) / std::max<std::size_t>(cols, 1));
-  std::vector<std::uint16_t> half;
+  std::vector<std::int32_t> half;
   for (std::size_t r0 = 0; r0 < rows; r0 += block) {
     const std::size_t r1 = std::min(rows, r0 + block);
     half.resize((r1 - r0) * cols);
     const ap_config c = dc.to_c(r0, r1);
-    check(ap_plot_dense(x.data.data(), x.size(), y.data.data(), y.size(), &c, half.data()));
+    check(ap_plot_dense_i32(x.data.data(), x.size(), y.data.data(), y.size(), &c, half.data()));
     for (std::size_t r = r0; r < r1; ++r)
-      for (std::size_t k = 0; k < cols; ++k)
-        emit(r, k, static_cast<half_score_t>(static_cast<std::int16_t>(half[(r - r0) * cols + k])));
+      for (std::size_t k = 0; k < cols; ++k) emit(r, k, half[(r - r0) * cols + k]);
   }
 }
 }  // namespace detail

@@ -187,15 +187,16 @@ __global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const uint32_t
 // Deterministic row-major placement of staged threshold records:
 // final index = offset[row * seg_stride + seg] + rank, where rows below split_row are cut into
 // segments of seg_cols columns and the rest (the launch's short tail tasks) of seg_cols2.
-// Structure-of-arrays output (orow/ocol/ohalf) or, with ocell != nullptr, ap_cell records
-// {row, col, int32 half} (PlotCell, scoring.hpp:33-42).
+// Structure-of-arrays output (orow/ocol and uint16 ohalf or int32 ohalf32) or, with
+// ocell != nullptr, ap_cell records {row, col, int32 half} (PlotCell, scoring.hpp:33-42).
 struct CellRec { uint32_t row, col; int32_t half; };
 
 __global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long nrec,
                              const unsigned long long* __restrict__ offsets, uint32_t seg_stride,
                              uint32_t seg_cols, uint32_t seg_cols2, uint32_t split_row, uint32_t r,
                              uint32_t row_global0, uint32_t* __restrict__ orow, uint32_t* __restrict__ ocol,
-                             uint16_t* __restrict__ ohalf, CellRec* __restrict__ ocell, unsigned long long cap) {
+                             uint16_t* __restrict__ ohalf, int32_t* __restrict__ ohalf32,
+                             CellRec* __restrict__ ocell, unsigned long long cap) {
   for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < nrec;
        i += 1ull * gridDim.x * blockDim.x) {
     const uint4 rec = stage[i];
@@ -204,14 +205,21 @@ __global__ void place_kernel(const uint4* __restrict__ stage, unsigned long long
     const unsigned long long pos = offsets[size_t(row) * seg_stride + seg] + rec.w;
     if (pos < cap) {
       if (ocell) {
-        ocell[pos] = CellRec{rec.x, rec.y, int32_t(int16_t(uint16_t(rec.z)))};
+        ocell[pos] = CellRec{rec.x, rec.y, int32_t(rec.z)};
       } else {
         orow[pos] = rec.x;
         ocol[pos] = rec.y;
-        ohalf[pos] = uint16_t(rec.z);
+        if (ohalf32) ohalf32[pos] = int32_t(rec.z);
+        else ohalf[pos] = uint16_t(rec.z);
       }
     }
   }
+}
+
+// uint16 half-units -> int32 (ap_plot_dense_i32 on the packed kernels, whose scores fit 16 bits)
+__global__ void widen_kernel(const uint16_t* __restrict__ in, size_t n, int32_t* __restrict__ out) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    out[i] = int32_t(in[i]);
 }
 
 }  // namespace apk

@@ -255,6 +255,8 @@ struct ap_ctx {
   uint32_t* h_small = nullptr;   // pinned mirror
   uint16_t* d_out = nullptr;
   size_t cap_out = 0;
+  uint16_t* d_out16 = nullptr;   // packed-kernel scores before widening to int32
+  size_t cap_out16 = 0;
   uint4* d_stage = nullptr;
   size_t cap_stage = 0;
   unsigned long long* d_cursor = nullptr;
@@ -355,6 +357,10 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
   return AP_OK;
 }
 
+// bytes per dense output entry: 0 = uint16 half-units, 1 = PGM pixels, 2 = uint8 half-units,
+// 3 = int32 half-units (PlotGrid's own type, model.hpp:95-114)
+size_t out_elem(int out_kind) { return out_kind == 0 ? 2 : out_kind == 3 ? 4 : 1; }
+
 // Thresholded runs: size the staging and the per-(row, segment) count buffers, zero the cursor.
 // Staging (one 16-B record per hit) is sized so a call normally stages every hit in one
 // pass: the grid's cell count bounds it, the caller's capacity is a floor, and otherwise it
@@ -425,6 +431,7 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   p.row_global0 = uint32_t(row_global0);
   p.out = static_cast<uint16_t*>(d_out);
   p.out8 = static_cast<uint8_t*>(d_out);
+  p.out32 = static_cast<int32_t*>(d_out);
   p.out_kind = uint32_t(out_kind);
   p.pgm_threshold = cfg->threshold_half;
   p.has_pgm_threshold = cfg->has_threshold ? 1u : 0u;
@@ -462,8 +469,7 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   std::snprintf(c->last_kernel, sizeof(c->last_kernel), "combw<%u,%d>", warps, apk::kWideRows);
   if (dense) {
     if (host_out) {
-      const size_t elem = out_kind == 0 ? 2 : 1;
-      CK(cudaMemcpyAsync(host_out, d_out, nrows * cols * elem, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(host_out, d_out, nrows * cols * out_elem(out_kind), cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
     return AP_OK;
@@ -527,6 +533,20 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const uint64_t skey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(out_kind) << 2) | (dense ? 1 : 0);
   const auto spec_hit = c->last_sigma.find(skey);
   const bool wide = W > AP_PACKED_WINDOW;   // the large-window path plans nothing by sigma
+  if (dense && out_kind == 3 && !wide) {
+    // int32 half-units on the packed kernels (scores < 2^16): uint16 into scratch, widened on the device
+    if ((rc = grow(&c->d_out16, &c->cap_out16, nrows * cols))) return rc;
+    if ((rc = run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, true, c->d_out16, st, nullptr, nullptr, 0, 0,
+                         nullptr, allow_spec)))
+      return rc;
+    apk::widen_kernel<<<unsigned(std::min<size_t>((nrows * cols + 255) / 256, size_t(c->sms) * 32)), 256, 0, st>>>(
+        c->d_out16, nrows * cols, static_cast<int32_t*>(d_out));
+    CK(cudaGetLastError());
+    c->last_launches += 1;
+    if (host_out) CK(cudaMemcpyAsync(host_out, d_out, nrows * cols * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return AP_OK;
+  }
   const bool speculate = !wide && allow_spec && !overrides && !std::getenv("AP_NO_SPEC") &&
                          spec_hit != c->last_sigma.end();
   // small inputs take the fused single-CTA code-stream kernel (one launch) when speculating
@@ -744,7 +764,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     //  * compute-bound (1-byte output): normal segments, ~16 equal row blocks of at least
     //    half a wave alternating over two compute streams (consecutive blocks overlap), so
     //    only the last block's copy is exposed.
-    const size_t elem = out_kind == 0 ? 2 : 1;
+    const size_t elem = out_elem(out_kind);
     const bool d2h_bound = double(elem) * 17.5 > 0.057 * double(W) * double(r);
     size_t Ss = d2h_bound ? std::max<size_t>(1024, 4 * size_t(W)) : S;
     if (const char* e = std::getenv("AP_STREAM_S")) Ss = std::max<size_t>(2 * W, std::strtoull(e, nullptr, 10));   // tuning
@@ -880,16 +900,26 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 // Place the list staged by the last thresholded run_device on c in row-major order
 // (apply_threshold, scoring.cpp:30-39): the first min(total, cap) cells into the device
 // arrays (rows/cols/halves, or ap_cell records when cells != nullptr).  Enqueued on st.
-int place_list(ap_ctx* c, cudaStream_t st, uint32_t* rows, uint32_t* cols, uint16_t* halves,
+int place_list(ap_ctx* c, cudaStream_t st, uint32_t* rows, uint32_t* cols, uint16_t* halves, int32_t* halves32,
                apk::CellRec* cells, size_t cap) {
   const ap_ctx::ListState& l = c->list;
   if (!l.nrec || !cap) return AP_OK;
   const size_t blocks = std::min<size_t>((l.nrec + 255) / 256, size_t(c->sms) * 16);
   apk::place_kernel<<<unsigned(blocks), 256, 0, st>>>(c->d_stage, l.nrec, c->d_offs, l.seg_stride, l.S, l.S2,
                                                         l.split_row, l.r, l.row_global0, rows, cols, halves,
-                                                        cells, cap);
+                                                        halves32, cells, cap);
   CK(cudaGetLastError());
   c->last_launches += 1;
+  return AP_OK;
+}
+
+// Half-unit scores lie in [0, 2w] (r = 1) or [0, 2w] with w <= 32767 (r = 2, W <= 65534), so
+// the uint16 entry points hold every score except LCS plots with w > 32767 (sea16 allows up to
+// 65534): those need the int32 forms (ap_plot_dense_i32, ap_plot_threshold_into / _cells).
+int check_u16(const ap_config* cfg) {
+  if (cfg && 2 * cfg->window_w > 65535 && cfg->blowup_r == 1)
+    return fail(AP_CONFIG, "scores of w = %zu reach %zu half-units, beyond uint16: use the int32 entry points",
+                size_t(cfg->window_w), size_t(2 * cfg->window_w));
   return AP_OK;
 }
 
@@ -972,7 +1002,8 @@ int ap_ctx_destroy(ap_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (void* p : {(void*)c->d_x, (void*)c->d_y, (void*)c->d_xcode, (void*)c->d_ycode, (void*)c->d_ycol, (void*)c->d_map,
                   (void*)c->d_small, (void*)c->d_tasks, (void*)c->d_out, (void*)c->d_stage, (void*)c->d_cursor,
-                  (void*)c->d_segc, (void*)c->d_offs, (void*)c->d_tsum, (void*)c->d_wkeys, (void*)c->d_wok})
+                  (void*)c->d_segc, (void*)c->d_offs, (void*)c->d_tsum, (void*)c->d_wkeys, (void*)c->d_wok,
+                  (void*)c->d_out16})
     if (p) cudaFree(p);
   if (c->pool) {
     cudaStreamSynchronize(c->stream_copy);
@@ -1013,7 +1044,7 @@ int ap_ctx_plot_dense_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint
                              const ap_config* cfg, uint16_t* d_out, void* stream) {
   if (!c || !d_x || !d_y || !d_out) return fail(AP_INVALID, "null argument");
   int rc = check_cfg(m, n, cfg);
-  if (rc) return rc;
+  if (rc || (rc = check_u16(cfg))) return rc;
   size_t rows, cols, rb, re;
   ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
   if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
@@ -1041,6 +1072,21 @@ int ap_ctx_plot_dense_u8_device(ap_ctx* c, const uint8_t* d_x, size_t m, const u
   return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr, nullptr, 0, 2);
 }
 
+int ap_ctx_plot_dense_i32_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
+                                 const ap_config* cfg, int32_t* d_out, void* stream) {
+  if (!c || !d_x || !d_y || !d_out) return fail(AP_INVALID, "null argument");
+  int rc = check_cfg(m, n, cfg);
+  if (rc) return rc;
+  size_t rows, cols, rb, re;
+  ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
+  if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DevGuard dg(c->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const size_t off = rb * cfg->step_h;
+  return run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, true, d_out, st, nullptr, nullptr, 0, 3);
+}
+
 int ap_ctx_plot_pgm_device(ap_ctx* c, const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n,
                            const ap_config* cfg, uint8_t* d_pixels, void* stream) {
   if (!c || !d_x || !d_y || !d_pixels) return fail(AP_INVALID, "null argument");
@@ -1063,7 +1109,7 @@ int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const 
   if (!c || !d_x || !d_y || !count) return fail(AP_INVALID, "null argument");
   if (cap && (!d_rows || !d_cols || !d_halves)) return fail(AP_INVALID, "null output arrays");
   int rc = check_cfg(m, n, cfg);
-  if (rc) return rc;
+  if (rc || (rc = check_u16(cfg))) return rc;
   size_t rows, cols, rb, re;
   ap_grid_dims(m, n, cfg->window_w, cfg->step_h, &rows, &cols);
   if ((rc = row_range(rows, cfg, &rb, &re))) return rc;
@@ -1074,7 +1120,7 @@ int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const 
   size_t nrec = 0, total = 0;
   rc = run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, false, nullptr, st, &nrec, &total, cap);
   if (rc) return rc;
-  if ((rc = place_list(c, st, d_rows, d_cols, d_halves, nullptr, cap))) return rc;
+  if ((rc = place_list(c, st, d_rows, d_cols, d_halves, nullptr, nullptr, cap))) return rc;
   CK(cudaStreamSynchronize(st));
   *count = total;
   if (total > cap) return fail(AP_CAPACITY, "%zu cells pass the threshold, capacity %zu", total, cap);
@@ -1179,7 +1225,7 @@ int host_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_
   int rc = plan_shards(x, m, y, n, cfg, &rb, &re, &cols, &sh);
   if (rc) return rc;
   if (!out && re > rb) return fail(AP_INVALID, "null output");
-  const size_t out_elem = out_kind == 0 ? 2 : 1;
+  const size_t elem = out_elem(out_kind);
   return for_shards(sh, [&](Shard& s) -> int {
     const size_t nrows = s.r1 - s.r0;
     if (nrows == 0) return AP_OK;
@@ -1190,9 +1236,9 @@ int host_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_
     size_t mx = 0;
     int q;
     if ((q = upload_shard(c, s, x, y, n, cfg, st, &mx))) return q;
-    if ((q = grow(&c->d_out, &c->cap_out, nrows * cols))) return q;
+    if ((q = grow(&c->d_out, &c->cap_out, nrows * cols * (out_kind == 3 ? 2 : 1)))) return q;
     if ((q = run_device(c, c->d_x, mx, c->d_y, n, cfg, nrows, s.r0, true, c->d_out, st, nullptr, nullptr, 0,
-                        out_kind, static_cast<char*>(out) + (s.r0 - rb) * cols * out_elem)))
+                        out_kind, static_cast<char*>(out) + (s.r0 - rb) * cols * elem)))
       return q;
     CK(cudaStreamSynchronize(st));
     return AP_OK;
@@ -1204,6 +1250,7 @@ struct ListDest {
   uint32_t* rows = nullptr;
   uint32_t* cols = nullptr;
   uint16_t* halves = nullptr;
+  int32_t* halves32 = nullptr;         // callback form: int32 scores
   ap_cell* cells = nullptr;            // array-of-structs form instead of rows / cols / halves
   size_t cap = 0;
   ap_list_alloc_fn alloc = nullptr;    // callback form: called once with the total
@@ -1221,7 +1268,7 @@ int host_list(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   std::vector<Shard> sh;
   int rc = plan_shards(x, m, y, n, cfg, &rb, &re, &cols, &sh);
   if (rc) return rc;
-  const size_t esz = dst.cells ? sizeof(ap_cell) : 2 * sizeof(uint32_t) + sizeof(uint16_t);
+  const size_t esz = dst.cells ? sizeof(ap_cell) : 2 * sizeof(uint32_t) + (dst.alloc ? 4 : 2);
   // entries a shard may need: its list starts at a global offset >= 0
   const size_t cap_any = dst.alloc ? ~size_t(0) : dst.cap;
   auto free_lists = [&]() {
@@ -1250,7 +1297,8 @@ int host_list(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
       CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&s.list), s.kept * esz, c->pool, st));
       uint32_t* lr = reinterpret_cast<uint32_t*>(s.list);
       if ((q = place_list(c, st, dst.cells ? nullptr : lr, dst.cells ? nullptr : lr + s.kept,
-                          dst.cells ? nullptr : reinterpret_cast<uint16_t*>(lr + 2 * s.kept),
+                          dst.cells || dst.alloc ? nullptr : reinterpret_cast<uint16_t*>(lr + 2 * s.kept),
+                          dst.alloc ? reinterpret_cast<int32_t*>(lr + 2 * s.kept) : nullptr,
                           dst.cells ? reinterpret_cast<apk::CellRec*>(s.list) : nullptr, s.kept)))
         return q;
     }
@@ -1271,11 +1319,11 @@ int host_list(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
   if (count) *count = total;
   size_t cap = dst.cap;
   if (dst.alloc) {
-    if (dst.alloc(dst.user, total, &dst.rows, &dst.cols, &dst.halves) != 0) {
+    if (dst.alloc(dst.user, total, &dst.rows, &dst.cols, &dst.halves32) != 0) {
       free_lists();
       return fail(AP_INVALID, "list allocation callback failed for %llu cells", (unsigned long long)total);
     }
-    if (total && (!dst.rows || !dst.cols || !dst.halves)) {
+    if (total && (!dst.rows || !dst.cols || !dst.halves32)) {
       free_lists();
       return fail(AP_INVALID, "list allocation callback returned null arrays");
     }
@@ -1292,7 +1340,10 @@ int host_list(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
       const uint32_t* lr = reinterpret_cast<const uint32_t*>(s.list);
       CK(cudaMemcpy(dst.rows + offs[d], lr, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(dst.cols + offs[d], lr + s.kept, k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(dst.halves + offs[d], lr + 2 * s.kept, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+      if (dst.alloc)
+        CK(cudaMemcpy(dst.halves32 + offs[d], lr + 2 * s.kept, k * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      else
+        CK(cudaMemcpy(dst.halves + offs[d], lr + 2 * s.kept, k * sizeof(uint16_t), cudaMemcpyDeviceToHost));
     }
     return AP_OK;
   });
@@ -1309,12 +1360,23 @@ extern "C" {
 
 int ap_plot_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                   uint16_t* out_half) {
+  if (int rc = check_u16(cfg)) return rc;
   if (cfg && cfg->has_threshold) {
     ap_config c = *cfg;   // the dense grid is never filtered (compute_plot, runner.cpp:78-131)
     c.has_threshold = 0;
     return host_dense(x, m, y, n, &c, out_half, 0);
   }
   return host_dense(x, m, y, n, cfg, out_half, 0);
+}
+
+int ap_plot_dense_i32(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
+                      int32_t* out_half) {
+  if (cfg && cfg->has_threshold) {
+    ap_config c = *cfg;
+    c.has_threshold = 0;
+    return host_dense(x, m, y, n, &c, out_half, 3);
+  }
+  return host_dense(x, m, y, n, cfg, out_half, 3);
 }
 
 int ap_plot_pgm(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
@@ -1339,6 +1401,7 @@ int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, co
   if (!count) return fail(AP_INVALID, "null count");
   if (cap && (!rows || !cols || !halves)) return fail(AP_INVALID, "null output arrays");
   if (!cfg || !cfg->has_threshold) return fail(AP_INVALID, "ap_plot_threshold needs has_threshold");
+  if (int rc = check_u16(cfg)) return rc;
   ListDest d;
   d.rows = rows;
   d.cols = cols;

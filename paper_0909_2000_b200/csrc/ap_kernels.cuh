@@ -92,7 +92,7 @@ struct CombParams {
   uint32_t has_pgm_threshold;
   // thresholded output
   int32_t t_half;
-  uint4* stage;                   // {row, col, half, rank} records
+  uint4* stage;                   // {row, col, int32 half, rank} records
   unsigned long long* cursor;     // staging append cursor
   uint32_t* task_counter;         // AP_DYN_TASKS: tasks handed out after the first static wave (zeroed per launch)
   unsigned long long stage_cap;
@@ -589,12 +589,12 @@ __device__ __forceinline__ void extract_out(const CombParams& p, uint32_t j, uin
         const uint32_t hb = imad(cab[c], 0xFFFFFFFEu, kb);
         const uint32_t hA = uint32_t(int32_t(hb & 0xFFFFu) - 0x8000), hB = uint32_t(int32_t(hb >> 16) - 0x8000);
         if ((hmA >> c) & 1u) {
-          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hA & 0xFFFFu, rkA);
+          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rA, gcol, hA, rkA);
           ++pos;
           ++rkA;
         }
         if ((hmB >> c) & 1u) {
-          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hB & 0xFFFFu, rkB);
+          if (pos < p.stage_cap) p.stage[pos] = make_uint4(p.row_global0 + rB, gcol, hB, rkB);
           ++pos;
           ++rkB;
         }

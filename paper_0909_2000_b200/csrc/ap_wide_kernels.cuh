@@ -55,7 +55,8 @@ struct WideParams {
   // dense output
   uint16_t* out;
   uint8_t* out8;
-  uint32_t out_kind;      // 0 = u16 half-units, 1 = PGM pixels, 2 = u8 half-units
+  int32_t* out32;
+  uint32_t out_kind;      // 0 = u16 half-units, 1 = PGM pixels, 2 = u8 half-units, 3 = int32 half-units
   int32_t pgm_threshold;
   uint32_t has_pgm_threshold;
   // thresholded output (the packed kernels' staging format; one segment per row)
@@ -212,6 +213,8 @@ __global__ void __launch_bounds__(kWideExtThreads) wide_extract_kernel(const Wid
         const size_t o = size_t(row) * p.cols + col;
         if (p.out_kind == 0) {
           p.out[o] = uint16_t(half);
+        } else if (p.out_kind == 3) {
+          p.out32[o] = half;
         } else if (p.out_kind == 2) {
           p.out8[o] = uint8_t(half);
         } else {   // write_pgm (io.cpp:136-153): (255 * clamp(h, 0, 2w) + w) / 2w, cut -> 0
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kWideExtThreads) wide_extract_kernel(const Wid
         if (hit) {
           const unsigned long long pos = base + rank;
           if (pos < p.stage_cap)
-            p.stage[pos] = make_uint4(p.row_global0 + row, col, uint32_t(half) & 0xFFFFu, hits_row + rank);
+            p.stage[pos] = make_uint4(p.row_global0 + row, col, uint32_t(half), hits_row + rank);
         }
         __syncthreads();
       }

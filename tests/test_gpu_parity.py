@@ -266,13 +266,15 @@ def test_forced_generic_fp16_keys_long(shape, w, r, monkeypatch):
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), shape
 
 
-def test_dense_u8_matches_u16():
+def test_dense_u8_and_i32_match_u16():
     rng = np.random.default_rng(8)
     x = rng.integers(1, 5, 600).astype(np.uint8)
     y = np.concatenate([x[50:350], rng.integers(1, 5, 400)]).astype(np.uint8)
     for w, h, r in ((100, 1, 2), (127, 2, 1), (30, 3, 2)):
         c = cfg(w, h, r)
         assert np.array_equal(ap.plot_dense_u8(x, y, c).astype(np.int32), gpu_grid(x, y, w, h, r))
+        assert np.array_equal(ap.plot_dense_i32(x, y, c), gpu_grid(x, y, w, h, r))
+        assert np.array_equal(ap.plot_dense_i32(x, y, c, 3, 9), gpu_grid(x, y, w, h, r)[3:9])
     with pytest.raises(ap.ConfigError):
         ap.plot_dense_u8(x, y, cfg(128, 1, 1))
 
@@ -747,8 +749,15 @@ def test_large_windows_vs_reference(w, r, h):
     y = np.concatenate([rng.integers(1, 5, 120), blk, rng.integers(1, 5, 180)]).astype(np.uint8)
     rc, want, err = ol.ref_compute_plot(x, y, w, h, r, ol.SEA16, os.cpu_count() or 8)
     assert rc == 0, err
-    got = gpu_grid(x, y, w, h, r)
+    got = ap.plot_dense_i32(x, y, cfg(w, h, r))
     assert got.shape == want.shape and np.array_equal(got, want), (w, r, h)
+    if ap.scores_fit_u16(cfg(w, h, r)):
+        assert np.array_equal(gpu_grid(x, y, w, h, r), want)
+    else:   # LCS scores up to 2w > 65535 half-units: the uint16 entry points refuse
+        with pytest.raises(ap.ConfigError):
+            gpu_grid(x, y, w, h, r)
+    grid = ap.compute_plot(ap.Sequence("x", x), ap.Sequence("y", y), cfg(w, h, r))
+    assert np.array_equal(grid.matrix(), want)
     t = int(np.quantile(want, 0.9))
     rr, cc = np.nonzero(want >= t)
     gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, h, r), t)

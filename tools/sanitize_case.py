@@ -33,3 +33,12 @@ yl = rng.integers(1, 5, 3000).astype(np.uint8)
 ap.plot_dense_u16(xl, yl, ap.PlotConfig(window_w=100, step_h=1, blowup_r=2, mode=ap.Mode.cuda))
 ap.plot_dense_u16(xl, yl, ap.PlotConfig(window_w=128, step_h=1, blowup_r=1, mode=ap.Mode.cuda))
 print("sanitize case (extended) ok")
+# the large-window path (w*r > 1024): band comb across 3 warps + prefix-sum extraction
+xw = rng.integers(1, 5, 1300).astype(np.uint8)
+yw = np.concatenate([xw[50:1250], rng.integers(1, 5, 300)]).astype(np.uint8)
+cw = ap.PlotConfig(window_w=1100, step_h=7, blowup_r=1, mode=ap.Mode.cuda)
+gw = ap.plot_dense_u16(xw, yw, cw)
+tw = int(np.quantile(gw, 0.9))
+assert ap.plot_threshold_arrays(xw, yw, cw, tw)[0].size == int((gw >= tw).sum())
+ap.plot_dense_u16(xw, yw, ap.PlotConfig(window_w=550, step_h=9, blowup_r=2, mode=ap.Mode.cuda))
+print("sanitize case (large window) ok")
