@@ -698,7 +698,7 @@ def test_threshold_into_single_pass_and_capacity_contract():
 
     def alloc(_u, n, pr, pc, ph):
         calls.append(int(n))
-        keep["a"] = [np.empty(max(n, 1), dt) for dt in (np.uint32, np.uint32, np.uint16)]
+        keep["a"] = [np.empty(max(n, 1), dt) for dt in (np.uint32, np.uint32, np.int32)]
         pr[0], pc[0], ph[0] = (a.ctypes.data for a in keep["a"])
         return 0
 
