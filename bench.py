@@ -53,7 +53,7 @@ from paper_0909_2000_b200.sharding import plan_row_shards, shard_x  # noqa: E402
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 INT_PEAK = os.path.join(ROOT, "profiles", "int_peak_r01.json")
-NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
 
 
 def log(*a):

@@ -227,6 +227,9 @@ constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: reba
 #ifndef AP_R2_SUBLOAD
 #define AP_R2_SUBLOAD 1   // r = 2 kernel, rolled sub loop: each sub prefetches its code words (no per-sub selects)
 #endif
+#ifndef AP_R2_PRMT
+#define AP_R2_PRMT 0   // r = 2 kernel: next code byte by one PRMT instead of SHF + LOP3
+#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -940,8 +943,14 @@ __device__ __forceinline__ void load_band_words(const uint4* tq, const uint32_t*
   }
 }
 
+#ifndef AP_R2_SHORT_WARPS
+#define AP_R2_SHORT_WARPS 16   // resident warps per SM the short-lane (RR < 8) r = 2 shapes are compiled for
+#endif
+__host__ __device__ constexpr int r2_min_blocks(int rr) {
+  return rr < 8 ? AP_R2_SHORT_WARPS / r2_wpc(rr) : (rr <= AP_R2_MB4 ? 4 : (rr <= 16 ? 3 : 2)) * 4 / r2_wpc(rr);
+}
 template <int L, int RR, int K, bool DENSE, bool HF>
-__global__ void __launch_bounds__(r2_wpc(RR) * 32, (RR <= AP_R2_MB4 ? 4 : (RR <= 16 ? 3 : 2)) * 4 / r2_wpc(RR))
+__global__ void __launch_bounds__(r2_wpc(RR) * 32, r2_min_blocks(RR))
 comb2_kernel(const CombParams p) {
   constexpr int WPC = r2_wpc(RR);
   static_assert(L <= 32 && RR % K == 0, "bad shape");
@@ -1164,7 +1173,11 @@ comb2_kernel(const CombParams p) {
           }
           {
             const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
+#if AP_R2_PRMT
+            const uint32_t ynew = __byte_perm(ww, 0u, 0x4440u | uint32_t((u + 1) & 3));   // one PRMT
+#else
             const uint32_t ynew = (ww >> (8 * ((u + 1) & 3))) & 0xFFu;
+#endif
             const uint32_t sh = shfl_up1<L>(cd[K - 1]);
 #pragma unroll
             for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
