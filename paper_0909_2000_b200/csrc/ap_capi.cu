@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
@@ -273,6 +275,11 @@ struct ap_ctx {
   uint8_t* d_wok = nullptr;     // large-window path: per-strip extraction flags
   size_t cap_wok = 0;
   cudaMemPool_t pool = nullptr;   // per-call list buffers of the host API (stream-ordered, cached)
+  // pinned bounce ring for device-to-host copies into pageable memory (allocated on first use)
+  static constexpr int kMaxBounceSlots = 16;
+  char* h_bounce = nullptr;
+  int bounce_slots = 0;
+  cudaEvent_t ev_bounce[kMaxBounceSlots] = {};
   // the staged list of the last thresholded run_device (placed by place_list)
   struct ListState {
     size_t nrec = 0;
@@ -354,6 +361,114 @@ int row_range(size_t rows, const ap_config* cfg, size_t* rb, size_t* re) {
   *re = cfg->row_end ? std::min<size_t>(cfg->row_end, rows) : rows;
   if (*rb > *re) return fail(AP_INVALID, "row_begin > row_end");
   if (*re - *rb > 0xFFFFFFF0ull) return fail(AP_INVALID, "too many rows in one call");
+  return AP_OK;
+}
+
+// ---- device-to-host copies of finished output ranges ----------------------------
+// A copy into pageable host memory is staged by the driver at ~21 GB/s on B200 hosts (57 GB/s
+// pinned, profiles/README_r02.md); callers of the host API (numpy arrays, std::vector) usually
+// pass pageable memory.  So pageable destinations go through a pinned ring of slots: the calling
+// thread issues slot-sized D2H copies on the copy stream as slots free up, and T host threads
+// copy finished slots to their destination in parallel (piece i -> slot i mod 2T -> thread
+// i mod T, so a thread only ever waits for copies it will itself release).
+struct CopyRange {
+  char* dst;
+  const char* src;
+  size_t bytes;
+  cudaEvent_t ready;   // the range is complete once this event fires (nullptr: already)
+};
+
+constexpr size_t kBounceSlotBytes = size_t(8) << 20;
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// All ranges copied when it returns.  Ranges must all be pinned or all pageable.
+int copy_out(ap_ctx* c, const std::vector<CopyRange>& rg) {
+  if (rg.empty()) return AP_OK;
+  if (host_pinned(rg[0].dst) || std::getenv("AP_NO_BOUNCE")) {
+    for (const CopyRange& r : rg) {
+      if (r.ready) CK(cudaStreamWaitEvent(c->stream_copy, r.ready, 0));
+      CK(cudaMemcpyAsync(r.dst, r.src, r.bytes, cudaMemcpyDeviceToHost, c->stream_copy));
+    }
+    CK(cudaStreamSynchronize(c->stream_copy));
+    return AP_OK;
+  }
+  if (!c->h_bounce) {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    c->bounce_slots = int(std::min<unsigned>(ap_ctx::kMaxBounceSlots, 2 * std::min(8u, hw / 2)));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_bounce), size_t(c->bounce_slots) * kBounceSlotBytes));
+    for (int k = 0; k < c->bounce_slots; ++k) CK(cudaEventCreateWithFlags(&c->ev_bounce[k], cudaEventDisableTiming));
+  }
+  struct Piece { char* dst; const char* src; size_t bytes; cudaEvent_t ready; };
+  std::vector<Piece> pcs;
+  for (const CopyRange& r : rg)
+    for (size_t off = 0; off < r.bytes; off += kBounceSlotBytes)
+      pcs.push_back({r.dst + off, r.src + off, std::min(kBounceSlotBytes, r.bytes - off), off ? nullptr : r.ready});
+  const size_t S = size_t(c->bounce_slots), T = S / 2, P = pcs.size();
+  std::mutex m;
+  std::condition_variable cv;
+  size_t issued = 0;
+  std::vector<size_t> freed(S);            // piece index that may use slot s next
+  for (size_t s2 = 0; s2 < S; ++s2) freed[s2] = s2;
+  std::atomic<int> err{AP_OK};
+  std::string err_msg;
+  auto worker = [&](size_t t) {
+    cudaSetDevice(c->device);
+    for (size_t i = t; i < P; i += T) {
+      {
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [&] { return issued > i || err.load() != AP_OK; });
+      }
+      if (err.load() != AP_OK) return;
+      const size_t s2 = i % S;
+      if (cudaEventSynchronize(c->ev_bounce[s2]) != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(m);
+        err = AP_CUDA;
+        err_msg = cudaGetErrorString(cudaGetLastError());
+        cv.notify_all();
+        return;
+      }
+      std::memcpy(pcs[i].dst, c->h_bounce + s2 * kBounceSlotBytes, pcs[i].bytes);
+      {
+        std::lock_guard<std::mutex> lk(m);
+        freed[s2] = i + S;
+      }
+      cv.notify_all();
+    }
+  };
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < std::min(T, P); ++t) th.emplace_back(worker, t);
+  for (size_t i = 0; i < P && err.load() == AP_OK; ++i) {
+    const size_t s2 = i % S;
+    {
+      std::unique_lock<std::mutex> lk(m);
+      cv.wait(lk, [&] { return freed[s2] >= i || err.load() != AP_OK; });
+    }
+    if (err.load() != AP_OK) break;
+    cudaError_t e = cudaSuccess;
+    if (pcs[i].ready) e = cudaStreamWaitEvent(c->stream_copy, pcs[i].ready, 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->h_bounce + s2 * kBounceSlotBytes, pcs[i].src, pcs[i].bytes, cudaMemcpyDeviceToHost,
+                          c->stream_copy);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_bounce[s2], c->stream_copy);
+    std::lock_guard<std::mutex> lk(m);
+    if (e != cudaSuccess) {
+      err = AP_CUDA;
+      err_msg = cudaGetErrorString(e);
+    } else {
+      issued = i + 1;
+    }
+    cv.notify_all();
+  }
+  for (auto& t : th) t.join();
+  if (err.load() != AP_OK) return fail(err.load(), "device-to-host copy: %s", err_msg.c_str());
   return AP_OK;
 }
 
@@ -469,7 +584,10 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   std::snprintf(c->last_kernel, sizeof(c->last_kernel), "combw<%u,%d>", warps, apk::kWideRows);
   if (dense) {
     if (host_out) {
-      CK(cudaMemcpyAsync(host_out, d_out, nrows * cols * out_elem(out_kind), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(c->ev_join, st));
+      if ((rc = copy_out(c, {{static_cast<char*>(host_out), static_cast<const char*>(d_out),
+                              nrows * cols * out_elem(out_kind), c->ev_join}})))
+        return rc;
     }
     CK(cudaStreamSynchronize(st));
     return AP_OK;
@@ -543,7 +661,12 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
         c->d_out16, nrows * cols, static_cast<int32_t*>(d_out));
     CK(cudaGetLastError());
     c->last_launches += 1;
-    if (host_out) CK(cudaMemcpyAsync(host_out, d_out, nrows * cols * 4, cudaMemcpyDeviceToHost, st));
+    if (host_out) {
+      CK(cudaEventRecord(c->ev_join, st));
+      if ((rc = copy_out(c, {{static_cast<char*>(host_out), static_cast<const char*>(d_out), nrows * cols * 4,
+                              c->ev_join}})))
+        return rc;
+    }
     CK(cudaStreamSynchronize(st));
     return AP_OK;
   }
@@ -817,13 +940,13 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     }
     // every block's kernel is enqueued before the first copy: a copy to pageable host memory
     // returns only when it is done, which would otherwise hold back the next block's launch
+    std::vector<CopyRange> ranges;
     for (size_t k = 0; k < nblk; ++k) {
       const size_t r0 = std::min(nrows, blk_g0[k] * 2 * G), r1 = std::min(nrows, blk_g0[k + 1] * 2 * G);
-      CK(cudaStreamWaitEvent(c->stream_copy, c->ev_blk[k], 0));
-      CK(cudaMemcpyAsync(static_cast<char*>(host_out) + r0 * cols * elem,
-                         static_cast<const char*>(d_out) + r0 * cols * elem, (r1 - r0) * cols * elem,
-                         cudaMemcpyDeviceToHost, c->stream_copy));
+      ranges.push_back({static_cast<char*>(host_out) + r0 * cols * elem,
+                        static_cast<const char*>(d_out) + r0 * cols * elem, (r1 - r0) * cols * elem, c->ev_blk[k]});
     }
+    if ((rc = copy_out(c, ranges))) return rc;
     if (!d2h_bound) {
       CK(cudaEventRecord(c->ev_join, c->stream_b));           // join the second stream
       CK(cudaStreamWaitEvent(st, c->ev_join, 0));
@@ -1009,6 +1132,8 @@ int ap_ctx_destroy(ap_ctx* c) {
     cudaStreamSynchronize(c->stream_copy);
     cudaMemPoolDestroy(c->pool);
   }
+  if (c->h_bounce) cudaFreeHost(c->h_bounce);
+  for (int k = 0; k < c->bounce_slots; ++k) cudaEventDestroy(c->ev_bounce[k]);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_cursor) cudaFreeHost(c->h_cursor);
   cudaStreamSynchronize(c->stream_copy);

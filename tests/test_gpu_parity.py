@@ -779,3 +779,32 @@ def test_large_window_many_rows_and_bound():
         ap.plot_dense_u16(np.ones(70000, np.uint8), np.ones(70000, np.uint8), cfg(65535, 1, 1))
     with pytest.raises(ap.ConfigError):
         ap.plot_dense_u16(np.ones(40000, np.uint8), np.ones(40000, np.uint8), cfg(32768, 1, 2))
+
+
+def test_dense_host_output_pinned_and_pageable_agree(monkeypatch):
+    """Dense host output into pageable memory goes through the pinned bounce ring (parallel host
+    copies); into pinned memory it is copied directly.  Both must give the oracle's grid, for
+    uint16, uint8 and int32 outputs and a plot larger than several bounce slots."""
+    import ctypes
+
+    import torch
+
+    from paper_0909_2000_b200 import _native
+    rng = np.random.default_rng(606)
+    x = rng.integers(1, 5, 3000).astype(np.uint8)
+    y = np.concatenate([x[200:2200], rng.integers(1, 5, 4000)]).astype(np.uint8)
+    w, h, r = 60, 1, 2
+    rows, cols = x.size - w + 1, y.size - w + 1      # 2941 x 5941: 35 MB of uint16
+    want = ap.plot_dense_u16(x, y, cfg(w, h, r))
+    monkeypatch.setenv("AP_NO_BOUNCE", "1")
+    assert np.array_equal(ap.plot_dense_u16(x, y, cfg(w, h, r)), want)
+    monkeypatch.delenv("AP_NO_BOUNCE")
+    pinned = torch.empty(rows * cols, dtype=torch.int16).pin_memory()
+    L = _native.lib()
+    c = ap._cfg(cfg(w, h, r))
+    assert L.ap_plot_dense(x.ctypes.data, x.size, y.ctypes.data, y.size, ctypes.byref(c), pinned.data_ptr()) == 0
+    assert np.array_equal(pinned.numpy().view(np.uint16).reshape(rows, cols), want)
+    assert np.array_equal(ap.plot_dense_i32(x, y, cfg(w, h, r)), want.astype(np.int32))
+    assert np.array_equal(ap.plot_dense_u8(x, y, cfg(w, h, r)), want.astype(np.uint8))
+    rc, ref_rows = ol.plot_rows(x, y, w, h, r, 1000, 1003)
+    assert rc == 0 and np.array_equal(want[1000:1003].astype(np.int32), ref_rows)
