@@ -392,7 +392,11 @@ bool host_pinned(const void* p) {
 // All ranges copied when it returns.  Ranges must all be pinned or all pageable.
 int copy_out(ap_ctx* c, const std::vector<CopyRange>& rg) {
   if (rg.empty()) return AP_OK;
-  if (host_pinned(rg[0].dst) || std::getenv("AP_NO_BOUNCE")) {
+  size_t total = 0;
+  for (const CopyRange& r : rg) total += r.bytes;
+  // below ~32 MB the ring's thread start-up costs more than the driver's staged copy saves
+  // (C1's 7.5 MB plot: 1.09 ms through the ring vs 0.68 ms direct)
+  if (total < (size_t(32) << 20) || host_pinned(rg[0].dst) || std::getenv("AP_NO_BOUNCE")) {
     for (const CopyRange& r : rg) {
       if (r.ready) CK(cudaStreamWaitEvent(c->stream_copy, r.ready, 0));
       CK(cudaMemcpyAsync(r.dst, r.src, r.bytes, cudaMemcpyDeviceToHost, c->stream_copy));

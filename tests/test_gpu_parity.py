@@ -791,10 +791,10 @@ def test_dense_host_output_pinned_and_pageable_agree(monkeypatch):
 
     from paper_0909_2000_b200 import _native
     rng = np.random.default_rng(606)
-    x = rng.integers(1, 5, 3000).astype(np.uint8)
-    y = np.concatenate([x[200:2200], rng.integers(1, 5, 4000)]).astype(np.uint8)
+    x = rng.integers(1, 5, 5000).astype(np.uint8)
+    y = np.concatenate([x[200:2200], rng.integers(1, 5, 6000)]).astype(np.uint8)
     w, h, r = 60, 1, 2
-    rows, cols = x.size - w + 1, y.size - w + 1      # 2941 x 5941: 35 MB of uint16
+    rows, cols = x.size - w + 1, y.size - w + 1      # 4941 x 7941: 78 MB of uint16 (10 bounce slots)
     want = ap.plot_dense_u16(x, y, cfg(w, h, r))
     monkeypatch.setenv("AP_NO_BOUNCE", "1")
     assert np.array_equal(ap.plot_dense_u16(x, y, cfg(w, h, r)), want)
@@ -806,5 +806,5 @@ def test_dense_host_output_pinned_and_pageable_agree(monkeypatch):
     assert np.array_equal(pinned.numpy().view(np.uint16).reshape(rows, cols), want)
     assert np.array_equal(ap.plot_dense_i32(x, y, cfg(w, h, r)), want.astype(np.int32))
     assert np.array_equal(ap.plot_dense_u8(x, y, cfg(w, h, r)), want.astype(np.uint8))
-    rc, ref_rows = ol.plot_rows(x, y, w, h, r, 1000, 1003)
-    assert rc == 0 and np.array_equal(want[1000:1003].astype(np.int32), ref_rows)
+    rc, ref_rows = ol.plot_rows(x, y, w, h, r, 4000, 4003)
+    assert rc == 0 and np.array_equal(want[4000:4003].astype(np.int32), ref_rows)
