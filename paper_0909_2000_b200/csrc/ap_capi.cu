@@ -527,13 +527,20 @@ int scan_counts(ap_ctx* c, size_t nc, cudaStream_t st) {
 // streams are already built (x codes, the $-interleaved y stream, $ code `sent`).
 int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, bool dense, void* d_out,
              cudaStream_t st, size_t* nrec_out, size_t* total_out, size_t cap, int out_kind, void* host_out,
-             uint32_t sent, size_t n) {
+             uint32_t sent, size_t n, uint32_t sigma_y) {
   const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
   const uint32_t W = w * r;
   const size_t N = n * r;
   const size_t cols = n - w + 1;
   int rc;
-  const uint32_t warps = std::min<uint32_t>(apk::kWideMaxWarps, (W + 32 * apk::kWideRows - 1) / (32 * apk::kWideRows));
+  // Computed masks: warps enough to hold the strip in one band (at most 32).  Mask table (alphabets
+  // of <= 8 codes, 2 KB per code and warp): 8-warp CTAs (4096-row bands), several per SM.
+  const uint32_t codes = sigma_y + (r == 2 ? 1u : 0u);
+  const bool tbl = !std::getenv("AP_WIDE_NO_TABLE") && codes <= 8;
+  const uint32_t warps = tbl ? 8u : std::min<uint32_t>(apk::kWideMaxWarps,
+                                                       (W + 32 * apk::kWideRows - 1) / (32 * apk::kWideRows));
+  const size_t wsmem = (tbl ? size_t(codes) * 32 * apk::kWideRows * 4 * warps : 0) +
+                       size_t(warps) * apk::kWideRing * 4;
   const uint32_t band_rows = warps * 32 * apk::kWideRows;
   apk::WideParams p{};
   p.xcode = c->d_xcode;
@@ -546,6 +553,10 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   p.sent_code = sent;
   p.band_rows = band_rows;
   p.bands = (W + band_rows - 1) / band_rows;
+  p.tbl_codes = codes;
+  CK(cudaFuncSetAttribute(tbl ? reinterpret_cast<const void*>(&apk::wide_comb_kernel<true>)
+                              : reinterpret_cast<const void*>(&apk::wide_comb_kernel<false>),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(wsmem)));
   p.cols = uint32_t(cols);
   p.row_global0 = uint32_t(row_global0);
   p.out = static_cast<uint16_t*>(d_out);
@@ -575,7 +586,8 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
       q.strips = uint32_t(std::min(batch, nrows - r0));
       q.row0 = uint32_t(r0);
       q.xcode = c->d_xcode + r0 * h;
-      apk::wide_comb_kernel<<<q.strips, warps * 32, 0, st>>>(q);
+      if (tbl) apk::wide_comb_kernel<true><<<q.strips, warps * 32, wsmem, st>>>(q);
+      else apk::wide_comb_kernel<false><<<q.strips, warps * 32, wsmem, st>>>(q);
       CK(cudaGetLastError());
       apk::wide_extract_kernel<<<q.strips, apk::kWideExtThreads, 0, st>>>(q);
       CK(cudaGetLastError());
@@ -585,7 +597,8 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   };
   if ((rc = launch_all())) return rc;
   CK(cudaEventRecord(c->ev1, st));
-  std::snprintf(c->last_kernel, sizeof(c->last_kernel), "combw<%u,%d>", warps, apk::kWideRows);
+  std::snprintf(c->last_kernel, sizeof(c->last_kernel), "combw<%u,%d,%s>", warps, apk::kWideRows,
+                tbl ? "table" : "computed");
   if (dense) {
     if (host_out) {
       CK(cudaEventRecord(c->ev_join, st));
@@ -716,7 +729,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaGetLastError());
     c->last_launches += 3;
     return run_wide(c, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out, cap, out_kind, host_out,
-                    sent, n);
+                    sent, n, sigma_y);
   }
 
   // launch plan (shape choice, function attributes, occupancy), cached per context;

@@ -49,6 +49,7 @@ struct WideParams {
   uint32_t h, w, r, W, N;
   uint32_t sent_code;     // $ code (r = 2)
   uint32_t bands, band_rows;   // bands per strip, rows per band (= threads * kWideRows)
+  uint32_t tbl_codes;          // TBL kernel: table codes (the y alphabet, plus $ for r = 2)
   uint32_t cols;          // grid columns
   uint32_t row0;          // launch row offset within the call (output row = row0 + strip)
   uint32_t row_global0;   // global grid row of the call's row 0
@@ -69,10 +70,18 @@ struct WideParams {
 };
 
 // One CTA per strip; blockDim.x = 32 * warps.
-__global__ void __launch_bounds__(1024, 1) wide_comb_kernel(const WideParams p) {
-  __shared__ int32_t ring[kWideMaxWarps][kWideRing];
+// TBL = true (alphabets of <= 8 codes, host-selected): 8-warp CTAs, several per SM, whose masks
+// come from a per-band table M[code][quad][thread] of int32 words (INT_MIN on a match, 0
+// otherwise; one LDS.128 per 4 rows, conflict-free); the cell is max(T + M, V) in one VIADDMNMX
+// plus the LOP3 -- 2 ALU ops per cell instead of 3 ALU + 2 FMA with computed masks.
+template <bool TBL>
+__global__ void __launch_bounds__(TBL ? 256 : 1024, 1) wide_comb_kernel(const WideParams p) {
+  // dynamic shared memory: TBL's table [codes][kWideRows / 4][threads] uint4, then the
+  // warp-to-warp rings [warps][kWideRing]
+  extern __shared__ __align__(16) unsigned char wsm[];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t nwarps = blockDim.x >> 5;
+  int32_t* ring = reinterpret_cast<int32_t*>(wsm + (TBL ? size_t(p.tbl_codes) * kWideRows * 4 * blockDim.x : 0));
   const uint32_t strip = blockIdx.x;
   const uint32_t N = p.N;
   int32_t* keys = p.keys + size_t(strip) * N;
@@ -81,6 +90,9 @@ __global__ void __launch_bounds__(1024, 1) wide_comb_kernel(const WideParams p) 
   const uint32_t nch = (N + 31 + kWideChunk - 1) / kWideChunk;
   const uint32_t nmacro = nch + 2 * (nwarps - 1);
   const uint32_t pad = p.bands * p.band_rows - p.W;   // never-matching rows above the strip
+  uint4* tb4 = reinterpret_cast<uint4*>(wsm);
+  constexpr int QW = kWideRows / 4;
+  const uint32_t code_stride = uint32_t(QW) * blockDim.x;   // uint4 per code
 
   for (uint32_t b = 0; b < p.bands; ++b) {
     // x codes of this thread's rows
@@ -99,11 +111,22 @@ __global__ void __launch_bounds__(1024, 1) wide_comb_kernel(const WideParams p) 
       }
       xr[rho] = int32_t(code);
     }
+    __syncthreads();    // the previous band's last bottom keys are written, its table reads done
+    if constexpr (TBL) {
+      for (uint32_t a = 0; a < p.tbl_codes; ++a)
+#pragma unroll
+        for (int q = 0; q < QW; ++q) {
+          uint32_t wv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) wv[k] = xr[4 * q + k] == int32_t(a) ? 0x80000000u : 0u;
+          tb4[a * code_stride + uint32_t(q) * blockDim.x + tid] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      __syncthreads();
+    }
     int32_t V[kWideRows];
 #pragma unroll
     for (int rho = 0; rho < kWideRows; ++rho) V[rho] = 0;   // left-boundary seaweeds
     int32_t tout = 0;   // seaweed leaving this thread's bottom row at the previous step
-    __syncthreads();    // the previous band's last bottom keys are written
 
     for (uint32_t k = 0; k < nmacro; ++k) {
       const int32_t lc = int32_t(k) - 2 * int32_t(warp);
@@ -119,24 +142,42 @@ __global__ void __launch_bounds__(1024, 1) wide_comb_kernel(const WideParams p) 
             // column s enters this warp: the strip's top (band 0: fresh key s + 1), the previous
             // band's bottom (keys[s]) or the warp above's bottom lane (ring)
             if (s < int32_t(N)) {
-              t = warp == 0 ? (b == 0 ? s + 1 : keys[s]) : ring[warp - 1][s & (kWideRing - 1)];
+              t = warp == 0 ? (b == 0 ? s + 1 : keys[s]) : ring[(warp - 1) * kWideRing + (s & (kWideRing - 1))];
             } else {
               t = 0;
             }
           }
+          if constexpr (TBL) {
+            // off-grid columns (c outside [0, N)) read code 0's words: t and V are still 0 there, so
+            // max(0 + M, 0) = 0 whatever M is
+            const uint4* tq = tb4 + uint32_t(valid ? yc : 0) * code_stride + tid;
 #pragma unroll
-          for (int rho = 0; rho < kWideRows; ++rho) {
-            int32_t dd, q1, tm, d;
-            asm("mad.lo.s32 %0, %1, -1, %2;" : "=r"(dd) : "r"(yc), "r"(xr[rho]));   // x - y (FMA pipe)
-            asm("mad.lo.s32 %0, %1, %1, -1;" : "=r"(q1) : "r"(dd));                 // < 0 iff x == y
-            asm("lop3.b32 %0, %1, %2, 0x80000000, 0x78;" : "=r"(tm) : "r"(t), "r"(q1));   // t ^ (q1 & 0x80000000)
-            d = max(tm, V[rho]);
-            V[rho] = V[rho] ^ t ^ d;
-            t = d;
+            for (int q = 0; q < QW; ++q) {
+              const uint4 m4 = tq[q * blockDim.x];
+              const uint32_t m[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const int rho = 4 * q + kk;
+                const int32_t d = __viaddmax_s32(t, int32_t(m[kk]), V[rho]);   // max(T + INT_MIN on a match, V)
+                V[rho] = V[rho] ^ t ^ d;
+                t = d;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int rho = 0; rho < kWideRows; ++rho) {
+              int32_t dd, q1, tm, d;
+              asm("mad.lo.s32 %0, %1, -1, %2;" : "=r"(dd) : "r"(yc), "r"(xr[rho]));   // x - y (FMA pipe)
+              asm("mad.lo.s32 %0, %1, %1, -1;" : "=r"(q1) : "r"(dd));                 // < 0 iff x == y
+              asm("lop3.b32 %0, %1, %2, 0x80000000, 0x78;" : "=r"(tm) : "r"(t), "r"(q1));   // t ^ (q1 & 0x80000000)
+              d = max(tm, V[rho]);
+              V[rho] = V[rho] ^ t ^ d;
+              t = d;
+            }
           }
           tout = t;
           if (lane == 31 && valid) {
-            if (warp + 1 < nwarps) ring[warp][c & (kWideRing - 1)] = t;
+            if (warp + 1 < nwarps) ring[warp * kWideRing + (c & (kWideRing - 1))] = t;
             else keys[c] = t;
           }
         }

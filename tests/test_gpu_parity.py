@@ -764,17 +764,26 @@ def test_large_windows_vs_reference(w, r, h):
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
 
 
-def test_large_window_many_rows_and_bound():
+@pytest.mark.parametrize("no_table", [False, True])
+def test_large_window_many_rows_and_bound(no_table, monkeypatch):
     """Large-window path over many rows (several strips per launch, both modes, row ranges)
-    against the oracle, and the sea16 bound: w*r = 65535 is a ConfigError before device work."""
+    against the oracle -- with the shared-memory mask table (alphabets of <= 8 codes, 4096-row
+    bands) and with computed masks (forced, and for a 20-letter alphabet) -- and the sea16 bound:
+    w*r = 65535 is a ConfigError before device work."""
+    if no_table:
+        monkeypatch.setenv("AP_WIDE_NO_TABLE", "1")
     rng = np.random.default_rng(1100)
-    for w, r in ((1100, 1), (600, 2)):
-        x = rng.integers(1, 5, w + 300).astype(np.uint8)
-        y = np.concatenate([x[100:w + 200], rng.integers(1, 5, 400)]).astype(np.uint8)
+    for w, r, sigma in ((1100, 1, 4), (600, 2, 4), (1500, 1, 20), (4200, 1, 3)):
+        x = rng.integers(1, sigma + 1, w + 300).astype(np.uint8)
+        y = np.concatenate([x[100:w + 200], rng.integers(1, sigma + 1, 400)]).astype(np.uint8)
         rc, want = ol.plot_rows(x, y, w, 1, r, 40, 140)
         assert rc == 0
         got = gpu_grid(x, y, w, 1, r, 40, 140)
-        assert np.array_equal(got, want), (w, r)
+        assert np.array_equal(got, want), (w, r, sigma)
+        t = int(np.quantile(want, 0.95))
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), t, row_begin=40, row_end=140)
+        assert np.array_equal(gr - 40, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
     with pytest.raises(ap.ConfigError):
         ap.plot_dense_u16(np.ones(70000, np.uint8), np.ones(70000, np.uint8), cfg(65535, 1, 1))
     with pytest.raises(ap.ConfigError):
