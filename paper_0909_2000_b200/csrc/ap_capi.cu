@@ -533,12 +533,13 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   const size_t N = n * r;
   const size_t cols = n - w + 1;
   int rc;
-  // Computed masks: warps enough to hold the strip in one band (at most 32).  Mask table (alphabets
-  // of <= 8 codes, 2 KB per code and warp): 8-warp CTAs (4096-row bands), several per SM.
+  // Warps per CTA: enough to hold the strip in one band (512 rows per warp), at most 32 with
+  // computed masks and at most 8 with the mask table (alphabets of <= 8 codes, 2 KB per code and
+  // warp; 4096-row bands, several CTAs per SM).
   const uint32_t codes = sigma_y + (r == 2 ? 1u : 0u);
   const bool tbl = !std::getenv("AP_WIDE_NO_TABLE") && codes <= 8;
-  const uint32_t warps = tbl ? 8u : std::min<uint32_t>(apk::kWideMaxWarps,
-                                                       (W + 32 * apk::kWideRows - 1) / (32 * apk::kWideRows));
+  const uint32_t warps = std::min<uint32_t>(tbl ? 8u : apk::kWideMaxWarps,
+                                            (W + 32 * apk::kWideRows - 1) / (32 * apk::kWideRows));
   const size_t wsmem = (tbl ? size_t(codes) * 32 * apk::kWideRows * 4 * warps : 0) +
                        size_t(warps) * apk::kWideRing * 4;
   const uint32_t band_rows = warps * 32 * apk::kWideRows;
