@@ -25,13 +25,20 @@ def main():
     a.add_argument("--n", type=int, default=400)
     a.add_argument("--seed", type=int, default=1)
     a.add_argument("--big", action="store_true", help="large windows (W up to 1024) and long y, few rows")
+    a.add_argument("--wide", action="store_true", help="blown windows 1025..8000 (the large-window path), few rows")
     args = a.parse_args()
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
     cells = 0
     for it in range(args.n):
         r = 1 + int(rng.integers(0, 2))
-        if args.big:
+        if args.wide:
+            w = int(rng.integers(1025, 8001)) // r
+            h = int(rng.choice([1, 1, 3]))
+            sigma = int(rng.choice([2, 4, 4, 20]))
+            m = int(rng.integers(w, w + 12))
+            n = int(rng.integers(w, w + 5000))
+        elif args.big:
             w = int(rng.integers(300, 1025 if r == 1 else 513))
             h = int(rng.choice([1, 1, 2]))
             sigma = int(rng.choice([4, 4, 20]))
@@ -54,7 +61,7 @@ def main():
         rc, want = ol.plot_rows(x, y, w, h, r)
         assert rc == 0
         c = ap.PlotConfig(window_w=w, step_h=h, blowup_r=r, mode=ap.Mode.cuda)
-        got = ap.plot_dense_u16(x, y, c).astype(np.int32)
+        got = ap.plot_dense_i32(x, y, c)
         assert np.array_equal(got, want), ("dense", it, w, h, r, m, y.size, sigma)
         t = int(np.quantile(want, 0.9))
         rr, cc, hh = ap.plot_threshold_arrays(x, y, c, t)
