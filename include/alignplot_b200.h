@@ -14,15 +14,21 @@
  * bindings.
  *
  * Scores are half-units (score x 2, reference model.hpp:13-15).  In both modes
- * a window-pair score lies in [0, 2w], so the engine stores uint16.
+ * a window-pair score lies in [0, 2w]: the uint16 entry points hold every score
+ * except LCS plots with w > 32767 (up to the sea16 bound w*r <= 65534), which
+ * take the int32 entry points (ap_plot_dense_i32, ap_plot_threshold_into,
+ * ap_plot_threshold_cells).
  * Output layout: row-major, out[row * cols + col] for grid row `row` (x-window
  * starting at row*h) and column `col` (y-window starting at col), exactly the
- * PlotGrid::values layout (model.hpp:95-114) narrowed from int32 to uint16.
+ * PlotGrid::values layout (model.hpp:95-114).
  *
- * Every entry point is reentrant; errors are status codes, and the message of
- * the calling thread's last failure is returned by ap_last_error().  There is
- * no CPU fallback: without a usable CUDA device every compute call returns
- * AP_NODEV.
+ * Every entry point is reentrant (calls on one device serialise on its
+ * context; a thresholded call's list lives in memory owned by the call until it
+ * is copied out); errors are status codes, and the message of the calling
+ * thread's last failure is returned by ap_last_error().  There is no CPU
+ * fallback: without a usable CUDA device every compute call returns AP_NODEV.
+ * Host output buffers may be pageable (large dense outputs then go through a
+ * pinned bounce ring) or pinned (copied directly). 
  */
 #ifndef ALIGNPLOT_B200_H
 #define ALIGNPLOT_B200_H
@@ -71,16 +77,17 @@ int ap_grid_dims(size_t m, size_t n, size_t w, size_t h, size_t* rows, size_t* c
 int ap_validate(size_t m, size_t n, const ap_config* cfg);
 
 /* Dense plot of grid rows [row_begin, row_end): out_half receives
- * (row_end-row_begin) * cols uint16 half-unit scores, row-major.
- * Replaces compute_plot (runner.cpp:78-131). */
+ * (row_end-row_begin) * cols uint16 half-unit scores, row-major (AP_CONFIG for
+ * LCS plots with w > 32767).  Replaces compute_plot (runner.cpp:78-131). */
 int ap_plot_dense(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                   uint16_t* out_half);
 
 /* Thresholded plot: the cells with half >= cfg->threshold_half, in row-major
  * order (apply_threshold, scoring.cpp:30-39), as three parallel arrays.
- * *count receives the total number of such cells; if it exceeds cap only the
- * first cap are written and AP_CAPACITY is returned.  Rows are grid rows
- * (global, i.e. counted from 0 even when row_begin > 0). */
+ * *count receives the total number of such cells (64-bit exact); if it exceeds
+ * cap only the first cap are written and AP_CAPACITY is returned (cap = 0 is a
+ * count-only query).  Rows are grid rows (global, i.e. counted from 0 even when
+ * row_begin > 0).  uint16 scores: AP_CONFIG for LCS plots with w > 32767. */
 int ap_plot_threshold(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_config* cfg,
                       uint64_t* count, uint32_t* rows, uint32_t* cols, uint16_t* halves,
                       size_t cap);
