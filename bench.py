@@ -157,7 +157,11 @@ def kernel_alu_ops_per_cell(kernel: str):
     if kernel.startswith("comb2"):
         return 5.0 / 8.0, "r=2 kernel: 5 ALU ops per 8 blown cells"
     if kernel.startswith("combw"):
-        return 2.0, f"large-window kernel {kernel}: 2 ALU ops per cell (32-bit keys)"
+        if kernel.endswith(",packed>"):
+            return 1.0, f"large-window kernel {kernel}: VIADDMNMX + LOP3 per two packed cells"
+        if ",table" in kernel:
+            return 2.0, f"large-window kernel {kernel}: VIADDMNMX + LOP3 per cell (32-bit keys)"
+        return 3.0, f"large-window kernel {kernel}: 3 ALU ops per cell (32-bit keys, computed masks)"
     ops = 5.0 if ",computed," in kernel else (1.75 if kernel.endswith("fp16>") else 2.0)
     return ops / 2.0, f"generic kernel {kernel}: {ops:g} ALU ops per 2 cells"
 

@@ -542,6 +542,10 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
                                             (W + 32 * apk::kWideRows - 1) / (32 * apk::kWideRows));
   const size_t wsmem = (tbl ? size_t(codes) * 32 * apk::kWideRows * 4 * warps : 0) +
                        size_t(warps) * apk::kWideRing * 4;
+  // Packed pairs (two strips per register, 16-bit keys) when the rebase step stays >= 96 columns:
+  // every seaweed a later window can count must survive a rebase (ap_wide_kernels.cuh)
+  const int32_t rebase_at = 0x7000, rebase_by = rebase_at - int32_t(W) - 64 * int32_t(warps) - 64;
+  const bool packed = tbl && rebase_by >= 96 && !std::getenv("AP_WIDE_NO_PACK");
   const uint32_t band_rows = warps * 32 * apk::kWideRows;
   apk::WideParams p{};
   p.xcode = c->d_xcode;
@@ -555,9 +559,12 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   p.band_rows = band_rows;
   p.bands = (W + band_rows - 1) / band_rows;
   p.tbl_codes = codes;
-  CK(cudaFuncSetAttribute(tbl ? reinterpret_cast<const void*>(&apk::wide_comb_kernel<true>)
-                              : reinterpret_cast<const void*>(&apk::wide_comb_kernel<false>),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(wsmem)));
+  p.rebase_at = uint32_t(rebase_at);
+  p.rebase_by = uint32_t(std::max(rebase_by, 0));
+  const void* wfn = packed ? reinterpret_cast<const void*>(&apk::wide2_comb_kernel)
+                            : tbl ? reinterpret_cast<const void*>(&apk::wide_comb_kernel<true>)
+                                  : reinterpret_cast<const void*>(&apk::wide_comb_kernel<false>);
+  CK(cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wsmem)));
   p.cols = uint32_t(cols);
   p.row_global0 = uint32_t(row_global0);
   p.out = static_cast<uint16_t*>(d_out);
@@ -575,7 +582,8 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
     p.stage_cap = c->cap_stage;
     p.seg_counts = c->d_segc;
   }
-  const size_t batch = std::max<size_t>(1, std::min<size_t>(nrows, (size_t(2) << 30) / (5 * N)));
+  size_t batch = std::max<size_t>(2, std::min<size_t>(nrows, (size_t(2) << 30) / (5 * N)));
+  batch += batch & 1;   // whole strip pairs per launch (packed kernel)
   if ((rc = grow(&c->d_wkeys, &c->cap_wkeys, batch * N))) return rc;
   if ((rc = grow(&c->d_wok, &c->cap_wok, batch * N))) return rc;
   p.keys = c->d_wkeys;
@@ -587,7 +595,8 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
       q.strips = uint32_t(std::min(batch, nrows - r0));
       q.row0 = uint32_t(r0);
       q.xcode = c->d_xcode + r0 * h;
-      if (tbl) apk::wide_comb_kernel<true><<<q.strips, warps * 32, wsmem, st>>>(q);
+      if (packed) apk::wide2_comb_kernel<<<(q.strips + 1) / 2, warps * 32, wsmem, st>>>(q);
+      else if (tbl) apk::wide_comb_kernel<true><<<q.strips, warps * 32, wsmem, st>>>(q);
       else apk::wide_comb_kernel<false><<<q.strips, warps * 32, wsmem, st>>>(q);
       CK(cudaGetLastError());
       apk::wide_extract_kernel<<<q.strips, apk::kWideExtThreads, 0, st>>>(q);
@@ -599,7 +608,7 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   if ((rc = launch_all())) return rc;
   CK(cudaEventRecord(c->ev1, st));
   std::snprintf(c->last_kernel, sizeof(c->last_kernel), "combw<%u,%d,%s>", warps, apk::kWideRows,
-                tbl ? "table" : "computed");
+                packed ? "table,packed" : tbl ? "table" : "computed");
   if (dense) {
     if (host_out) {
       CK(cudaEventRecord(c->ev_join, st));

@@ -50,6 +50,7 @@ struct WideParams {
   uint32_t sent_code;     // $ code (r = 2)
   uint32_t bands, band_rows;   // bands per strip, rows per band (= threads * kWideRows)
   uint32_t tbl_codes;          // TBL kernel: table codes (the y alphabet, plus $ for r = 2)
+  uint32_t rebase_at, rebase_by;   // packed kernel: relative-key bound and rebase step
   uint32_t cols;          // grid columns
   uint32_t row0;          // launch row offset within the call (output row = row0 + strip)
   uint32_t row_global0;   // global grid row of the call's row 0
@@ -179,6 +180,137 @@ __global__ void __launch_bounds__(TBL ? 256 : 1024, 1) wide_comb_kernel(const Wi
           if (lane == 31 && valid) {
             if (warp + 1 < nwarps) ring[warp * kWideRing + (c & (kWideRing - 1))] = t;
             else keys[c] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Packed variant (alphabets of <= 8 codes and W up to ~28K; host-selected): one CTA per strip
+// PAIR (grid rows 2p, 2p+1 of the launch, same y columns) with both strips' 16-bit start keys in
+// one register and the packed kernels' cell -- VIADDMNMX.S16x2 + LOP3 for two cells -- from table
+// words carrying both strips' match bits (15, 31).  Keys are relative to a CTA-wide base and are
+// rebased (saturating at 0) at macro-step boundaries by every thread at once, so all keys in
+// flight (registers, the warp-to-warp ring) shift together; p.rebase_by keeps every seaweed a
+// later window can count unsaturated (host: by = 0x7000 - W - 64 * warps - 64).  The bottom keys
+// leave as absolute int32 starts (+1) per strip, as the 32-bit kernel writes them.
+__global__ void __launch_bounds__(256, 1) wide2_comb_kernel(const WideParams p) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t nwarps = blockDim.x >> 5;
+  const uint32_t sa = 2 * blockIdx.x, sb = sa + 1;
+  const bool has_b = sb < p.strips;
+  const uint32_t N = p.N;
+  int32_t* keys_a = p.keys + size_t(sa) * N;
+  int32_t* keys_b = p.keys + size_t(has_b ? sb : sa) * N;
+  const uint8_t* xa_row = p.xcode + size_t(sa) * p.h;
+  const uint8_t* xb_row = p.xcode + size_t(has_b ? sb : sa) * p.h;
+  const uint32_t rshift = p.r - 1;
+  const uint32_t nch = (N + 31 + kWideChunk - 1) / kWideChunk;
+  const uint32_t nmacro = nch + 2 * (nwarps - 1);
+  const uint32_t pad = p.bands * p.band_rows - p.W;
+  constexpr int QW = kWideRows / 4;
+  uint4* tb4 = reinterpret_cast<uint4*>(wsm);
+  const uint32_t code_stride = uint32_t(QW) * blockDim.x;
+  uint32_t* ring = reinterpret_cast<uint32_t*>(wsm + size_t(p.tbl_codes) * kWideRows * 4 * blockDim.x);
+  const uint32_t by2 = p.rebase_by * 0x00010001u;
+
+  for (uint32_t b = 0; b < p.bands; ++b) {
+    uint32_t xa[kWideRows], xb[kWideRows];
+#pragma unroll
+    for (int rho = 0; rho < kWideRows; ++rho) {
+      const int32_t i = int32_t(b * p.band_rows + tid * kWideRows + rho) - int32_t(pad);
+      uint32_t ca = kPadCode, cb = kPadCode;
+      if (i >= 0) {
+        if (p.r == 2 && !(i & 1)) {
+          ca = p.sent_code;
+          cb = has_b ? p.sent_code : kPadCode;
+        } else {
+          ca = xa_row[uint32_t(i) >> rshift];
+          cb = has_b ? xb_row[uint32_t(i) >> rshift] : kPadCode;
+          if (ca == 0xFFu) ca = kPadCode;
+          if (cb == 0xFFu) cb = kPadCode;
+        }
+      }
+      xa[rho] = ca;
+      xb[rho] = cb;
+    }
+    __syncthreads();   // the previous band's bottom keys are written, its table reads done
+    for (uint32_t a = 0; a < p.tbl_codes; ++a)
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          wv[k] = (xa[4 * q + k] == a ? 0x00008000u : 0u) | (xb[4 * q + k] == a ? 0x80000000u : 0u);
+        tb4[a * code_stride + uint32_t(q) * blockDim.x + tid] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+    __syncthreads();
+    uint32_t V[kWideRows];
+#pragma unroll
+    for (int rho = 0; rho < kWideRows; ++rho) V[rho] = 0u;
+    uint32_t tout = 0u;
+    int32_t kbase = 0;   // key = absolute start + 1 - kbase (0: left boundary or saturated)
+
+    for (uint32_t k = 0; k < nmacro; ++k) {
+      if (int32_t(32 * (k + 2)) - kbase >= int32_t(p.rebase_at)) {   // uniform over the CTA
+#pragma unroll
+        for (int rho = 0; rho < kWideRows; ++rho) V[rho] = __vmaxu2(V[rho], by2) - by2;
+        tout = __vmaxu2(tout, by2) - by2;
+        for (uint32_t q = tid; q < nwarps * kWideRing; q += blockDim.x) ring[q] = __vmaxu2(ring[q], by2) - by2;
+        kbase += int32_t(p.rebase_by);
+        __syncthreads();
+      }
+      const int32_t lc = int32_t(k) - 2 * int32_t(warp);
+      if (lc >= 0 && uint32_t(lc) < nch) {
+        for (int u = 0; u < kWideChunk; ++u) {
+          const int32_t s = lc * kWideChunk + u;
+          const int32_t c = s - int32_t(lane);
+          const bool valid = c >= 0 && c < int32_t(N);
+          const uint32_t yc = valid ? uint32_t(__ldg(p.ycode + c)) : 0u;
+          const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, tout, 1);
+          uint32_t t = sh;
+          if (lane == 0) {
+            if (s < int32_t(N)) {
+              if (warp == 0) {
+                if (b == 0) {
+                  t = uint32_t(s + 1 - kbase) * 0x00010001u;   // fresh: >= 1 (host bound on rebase_by)
+                } else {
+                  const int32_t ka = max(keys_a[s] - kbase, 0), kb = max(keys_b[s] - kbase, 0);
+                  t = uint32_t(ka) | (uint32_t(kb) << 16);
+                }
+              } else {
+                t = ring[(warp - 1) * kWideRing + (s & (kWideRing - 1))];
+              }
+            } else {
+              t = 0u;
+            }
+          }
+          // off-grid columns: t and V are 0, and max(0 + M, 0) = 0 whatever M is
+          const uint4* tq = tb4 + yc * code_stride + tid;
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const uint4 m4 = tq[q * blockDim.x];
+            const uint32_t m[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint32_t& v = V[4 * q + kk];
+              const uint32_t d = __viaddmax_s16x2(t, m[kk], v);   // max(T + A, V): A = -32768 on a match
+              v = v ^ t ^ d;
+              t = d;
+            }
+          }
+          tout = t;
+          if (lane == 31 && valid) {
+            if (warp + 1 < nwarps) {
+              ring[warp * kWideRing + (c & (kWideRing - 1))] = t;
+            } else {
+              const uint32_t ka = t & 0xFFFFu, kb = t >> 16;
+              keys_a[c] = ka ? int32_t(ka) + kbase : 0;
+              if (has_b) keys_b[c] = kb ? int32_t(kb) + kbase : 0;
+            }
           }
         }
       }

@@ -17,7 +17,9 @@ def test_kernel_alu_ops_follow_the_chosen_kernel():
     assert bench.kernel_alu_ops_per_cell("comb<4,32,2,table,fp16>")[0] == 1.75 / 2
     assert bench.kernel_alu_ops_per_cell("comb<8,8,2,table,int>")[0] == 1.0
     assert bench.kernel_alu_ops_per_cell("comb<8,16,4,computed,int>")[0] == 2.5
-    assert bench.kernel_alu_ops_per_cell("combw<32,32>")[0] == 2.0
+    assert bench.kernel_alu_ops_per_cell("combw<8,16,table,packed>")[0] == 1.0
+    assert bench.kernel_alu_ops_per_cell("combw<8,16,table>")[0] == 2.0
+    assert bench.kernel_alu_ops_per_cell("combw<32,16,computed>")[0] == 3.0
 
 
 def test_default_scaling_per_config():

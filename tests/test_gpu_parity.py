@@ -764,17 +764,20 @@ def test_large_windows_vs_reference(w, r, h):
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
 
 
-@pytest.mark.parametrize("no_table", [False, True])
-def test_large_window_many_rows_and_bound(no_table, monkeypatch):
-    """Large-window path over many rows (several strips per launch, both modes, row ranges)
-    against the oracle -- with the shared-memory mask table (alphabets of <= 8 codes, 4096-row
-    bands) and with computed masks (forced, and for a 20-letter alphabet) -- and the sea16 bound:
-    w*r = 65535 is a ConfigError before device work."""
-    if no_table:
+@pytest.mark.parametrize("variant", ["default", "no_pack", "no_table"])
+def test_large_window_many_rows_and_bound(variant, monkeypatch):
+    """Large-window path over many rows (several strips per launch, odd row counts, both modes,
+    row ranges) against the oracle, in all three kernels: packed strip pairs with 16-bit keys and
+    CTA-wide rebasing (the default for alphabets of <= 8 codes and W up to ~28K), 32-bit keys with
+    the mask table (AP_WIDE_NO_PACK), computed masks (AP_WIDE_NO_TABLE, and a 20-letter alphabet);
+    and the sea16 bound: w*r = 65535 is a ConfigError before device work."""
+    if variant == "no_pack":
+        monkeypatch.setenv("AP_WIDE_NO_PACK", "1")
+    if variant == "no_table":
         monkeypatch.setenv("AP_WIDE_NO_TABLE", "1")
     rng = np.random.default_rng(1100)
     for w, r, sigma in ((1100, 1, 4), (600, 2, 4), (1500, 1, 20), (4200, 1, 3)):
-        x = rng.integers(1, sigma + 1, w + 300).astype(np.uint8)
+        x = rng.integers(1, sigma + 1, w + 300).astype(np.uint8)   # 301 rows: the last pair is half
         y = np.concatenate([x[100:w + 200], rng.integers(1, sigma + 1, 400)]).astype(np.uint8)
         rc, want = ol.plot_rows(x, y, w, 1, r, 40, 140)
         assert rc == 0
@@ -817,3 +820,19 @@ def test_dense_host_output_pinned_and_pageable_agree(monkeypatch):
     assert np.array_equal(ap.plot_dense_u8(x, y, cfg(w, h, r)), want.astype(np.uint8))
     rc, ref_rows = ol.plot_rows(x, y, w, h, r, 4000, 4003)
     assert rc == 0 and np.array_equal(want[4000:4003].astype(np.int32), ref_rows)
+
+
+def test_large_window_packed_rebases_over_long_y():
+    """The packed large-window kernel rebases its 16-bit keys every (0x7000 - W - 64 warps - 64)
+    columns; over a y of 120K columns at W = 20000 (rebase step 8096, ~15 rebases) and W = 2000 with
+    r = 2 (W = 4000), planted homology far from the start must still give the oracle's rows."""
+    rng = np.random.default_rng(7070)
+    for w, r, n in ((20000, 1, 120000), (2000, 2, 60000)):
+        x = rng.integers(1, 5, w + 3).astype(np.uint8)
+        blk = x[:w].copy()
+        flip = rng.random(w) < 0.1
+        blk[flip] = rng.integers(1, 5, int(flip.sum()))
+        y = np.concatenate([rng.integers(1, 5, n - w - 500), blk, rng.integers(1, 5, 500)]).astype(np.uint8)
+        rc, want, err = ol.ref_compute_plot(x, y, w, 1, r, ol.SEA16, 16)
+        assert rc == 0, err
+        assert np.array_equal(ap.plot_dense_i32(x, y, cfg(w, 1, r)), want), (w, r)

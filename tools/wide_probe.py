@@ -42,7 +42,7 @@ def main():
         ms = L.ap_ctx_last_kernel_ms(ctx)
         cells = rows * (w * r) * (y.size * r)
         kern = (L.ap_ctx_last_kernel(ctx) or b"").decode()
-        ops = 2.0 if ",table" in kern else 3.0
+        ops = 1.0 if kern.endswith(",packed>") else 2.0 if ",table" in kern else 3.0
         frac = cells * ops / (ms / 1e3) / (148 * 63.41 * 1.965e9)
         print(f"w={w} r={r} sigma={alpha.size} rows={rows} n={y.size} kernel={kern} {ms:.2f} ms "
               f"{cells / (ms / 1e3):.3e} comb cells/s, ALU-op frac {frac:.3f}", flush=True)
