@@ -265,34 +265,54 @@ __global__ void __launch_bounds__(256, 1) wide2_comb_kernel(const WideParams p) 
       }
       const int32_t lc = int32_t(k) - 2 * int32_t(warp);
       if (lc >= 0 && uint32_t(lc) < nch) {
+        // branch-free per step: codes by clamped loads (the stream has >= 256 pad bytes) and a
+        // select; the column entering this warp is formed by every lane (warp-uniform branches,
+        // broadcast loads) and taken by lane 0 with one select
+        auto code_at = [&](int32_t cc) -> uint32_t {
+          const uint32_t v = uint32_t(__ldg(p.ycode + min(max(cc, 0), int32_t(N))));
+          return cc >= 0 && cc < int32_t(N) ? v : 0u;
+        };
+        const int32_t c0 = lc * kWideChunk - int32_t(lane);
+        uint32_t yc_next = code_at(c0 + 1);
+        uint4 mq[QW];
+        {
+          const uint4* tq = tb4 + code_at(c0) * code_stride + tid;
+#pragma unroll
+          for (int q = 0; q < QW; ++q) mq[q] = tq[q * blockDim.x];
+        }
+        const uint32_t* ring_in = ring + (warp ? warp - 1 : 0) * kWideRing;
+        uint32_t* ring_out = ring + warp * kWideRing;
+        const bool last_warp = warp + 1 == nwarps;
+#pragma unroll 2
         for (int u = 0; u < kWideChunk; ++u) {
           const int32_t s = lc * kWideChunk + u;
           const int32_t c = s - int32_t(lane);
           const bool valid = c >= 0 && c < int32_t(N);
-          const uint32_t yc = valid ? uint32_t(__ldg(p.ycode + c)) : 0u;
+          const uint32_t yc_after = code_at(c + 2);
           const uint32_t sh = __shfl_up_sync(0xFFFFFFFFu, tout, 1);
-          uint32_t t = sh;
-          if (lane == 0) {
-            if (s < int32_t(N)) {
-              if (warp == 0) {
-                if (b == 0) {
-                  t = uint32_t(s + 1 - kbase) * 0x00010001u;   // fresh: >= 1 (host bound on rebase_by)
-                } else {
-                  const int32_t ka = max(keys_a[s] - kbase, 0), kb = max(keys_b[s] - kbase, 0);
-                  t = uint32_t(ka) | (uint32_t(kb) << 16);
-                }
-              } else {
-                t = ring[(warp - 1) * kWideRing + (s & (kWideRing - 1))];
-              }
-            } else {
-              t = 0u;
-            }
+          uint32_t inj;                      // the seaweed pair entering this warp at column s
+          if (warp != 0) {
+            inj = ring_in[s & (kWideRing - 1)];
+          } else if (b == 0) {
+            inj = uint32_t(s + 1 - kbase) * 0x00010001u;   // fresh: >= 1 (host bound on rebase_by)
+          } else {
+            const int32_t sc = min(s, int32_t(N) - 1);
+            inj = uint32_t(max(keys_a[sc] - kbase, 0)) | (uint32_t(max(keys_b[sc] - kbase, 0)) << 16);
           }
+          uint32_t t = lane == 0 ? (s < int32_t(N) ? inj : 0u) : sh;
           // off-grid columns: t and V are 0, and max(0 + M, 0) = 0 whatever M is
-          const uint4* tq = tb4 + yc * code_stride + tid;
+          uint4 mcur[QW];
+#pragma unroll
+          for (int q = 0; q < QW; ++q) mcur[q] = mq[q];
+          {
+            const uint4* tq = tb4 + yc_next * code_stride + tid;   // the next step's words
+#pragma unroll
+            for (int q = 0; q < QW; ++q) mq[q] = tq[q * blockDim.x];
+          }
+          yc_next = yc_after;
 #pragma unroll
           for (int q = 0; q < QW; ++q) {
-            const uint4 m4 = tq[q * blockDim.x];
+            const uint4 m4 = mcur[q];
             const uint32_t m[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
@@ -303,14 +323,12 @@ __global__ void __launch_bounds__(256, 1) wide2_comb_kernel(const WideParams p) 
             }
           }
           tout = t;
-          if (lane == 31 && valid) {
-            if (warp + 1 < nwarps) {
-              ring[warp * kWideRing + (c & (kWideRing - 1))] = t;
-            } else {
-              const uint32_t ka = t & 0xFFFFu, kb = t >> 16;
-              keys_a[c] = ka ? int32_t(ka) + kbase : 0;
-              if (has_b) keys_b[c] = kb ? int32_t(kb) + kbase : 0;
-            }
+          if (!last_warp) {
+            if (lane == 31 && valid) ring_out[c & (kWideRing - 1)] = t;
+          } else if (lane == 31 && valid) {
+            const uint32_t ka = t & 0xFFFFu, kb = t >> 16;
+            keys_a[c] = ka ? int32_t(ka) + kbase : 0;
+            if (has_b) keys_b[c] = kb ? int32_t(kb) + kbase : 0;
           }
         }
       }
