@@ -487,9 +487,9 @@ size_t out_elem(int out_kind) { return out_kind == 0 ? 2 : out_kind == 3 ? 4 : 1
 // than the staging still comes out exact: the kernel counts every hit, the staging grows to
 // the exact size and the comb re-runs (rare).
 int stage_prepare(ap_ctx* c, size_t nrows, size_t cols, size_t cap, size_t seg_stride, bool zero_counts,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool count_only = false) {
   int rc;
-  const size_t cells_ub = nrows * cols + 1;
+  const size_t cells_ub = count_only ? 1 : nrows * cols + 1;   // a count-only call stages nothing
   size_t target = std::max(std::min(cells_ub, size_t(1) << 28), std::min(cap, cells_ub));
   if (c->cap_stage < target) {
     size_t fr = 0, tot = 0;
@@ -527,7 +527,7 @@ int scan_counts(ap_ctx* c, size_t nc, cudaStream_t st) {
 // streams are already built (x codes, the $-interleaved y stream, $ code `sent`).
 int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, bool dense, void* d_out,
              cudaStream_t st, size_t* nrec_out, size_t* total_out, size_t cap, int out_kind, void* host_out,
-             uint32_t sent, size_t n, uint32_t sigma_y) {
+             uint32_t sent, size_t n, uint32_t sigma_y, bool count_only) {
   const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
   const uint32_t W = w * r;
   const size_t N = n * r;
@@ -575,11 +575,11 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   p.has_pgm_threshold = cfg->has_threshold ? 1u : 0u;
   p.dense = dense ? 1u : 0u;
   if (!dense) {
-    if ((rc = stage_prepare(c, nrows, cols, cap, 1, false, st))) return rc;
+    if ((rc = stage_prepare(c, nrows, cols, cap, 1, false, st, count_only))) return rc;
     p.t_half = cfg->threshold_half;
     p.stage = c->d_stage;
     p.cursor = c->d_cursor;
-    p.stage_cap = c->cap_stage;
+    p.stage_cap = count_only ? 0 : c->cap_stage;
     p.seg_counts = c->d_segc;
   }
   size_t batch = std::max<size_t>(2, std::min<size_t>(nrows, (size_t(2) << 30) / (5 * N)));
@@ -623,14 +623,14 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
   CK(cudaStreamSynchronize(st));
   const size_t nrec = c->h_cursor[0], total = c->h_cursor[1];
   if (nrec != total) return fail(AP_CUDA, "threshold bookkeeping mismatch (%zu staged vs %zu counted)", nrec, total);
-  if (nrec > c->cap_stage) {   // staging overflowed: grow to the exact size and recompute (rare)
+  if (nrec > c->cap_stage && !count_only) {   // staging overflowed: grow to the exact size and recompute (rare)
     if ((rc = grow(&c->d_stage, &c->cap_stage, nrec))) return rc;
     p.stage = c->d_stage;
     p.stage_cap = c->cap_stage;
     CK(cudaMemsetAsync(c->d_cursor, 0, sizeof(unsigned long long), st));
     if ((rc = launch_all())) return rc;
   }
-  c->list.nrec = nrec;
+  c->list.nrec = count_only ? 0 : nrec;
   c->list.seg_stride = 1;
   c->list.S = uint32_t(N + 1);   // one segment per row
   c->list.S2 = uint32_t(N + 1);
@@ -651,11 +651,13 @@ int run_wide(ap_ctx* c, const ap_config* cfg, size_t nrows, size_t row_global0, 
 #endif
 
 // Thresholded runs (dense = false) stage the hits and leave them in c->list for place_list;
-// `cap` is the caller's list capacity (a lower bound for the staging size).
+// `cap` is the caller's list capacity (a lower bound for the staging size).  count_only: the
+// caller wants the count alone, so a staging overflow is not re-run (the count is exact anyway).
 int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, size_t n,
                const ap_config* cfg, size_t nrows, size_t row_global0, bool dense,
                void* d_out, cudaStream_t st, size_t* nrec_out, size_t* total_out,
-               size_t cap, int out_kind = 0, void* host_out = nullptr, bool allow_spec = true) {
+               size_t cap, int out_kind = 0, void* host_out = nullptr, bool allow_spec = true,
+               bool count_only = false) {
   const uint32_t w = uint32_t(cfg->window_w), h = uint32_t(cfg->step_h), r = cfg->blowup_r;
   const uint32_t W = w * r;
   const size_t N = n * r;
@@ -739,7 +741,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaGetLastError());
     c->last_launches += 3;
     return run_wide(c, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out, cap, out_kind, host_out,
-                    sent, n, sigma_y);
+                    sent, n, sigma_y, count_only);
   }
 
   // launch plan (shape choice, function attributes, occupancy), cached per context;
@@ -885,13 +887,13 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   if (!dense) {
     // with a tail split the rows of the long-task groups leave counts nseg..seg_stride-1 unset
-    if ((rc = stage_prepare(c, nrows, cols, cap, p.seg_stride, p.seg_stride != p.nseg, st))) return rc;
+    if ((rc = stage_prepare(c, nrows, cols, cap, p.seg_stride, p.seg_stride != p.nseg, st, count_only))) return rc;
     // the kernel tests h >= t in biased 16-bit halves: |h| <= 2048, so clamping t
     // to +-0x4000 keeps every comparison exact
     p.t_half = std::min<int32_t>(0x4000, std::max<int32_t>(-0x4000, cfg->threshold_half));
     p.stage = c->d_stage;
     p.cursor = c->d_cursor;
-    p.stage_cap = c->cap_stage;
+    p.stage_cap = count_only ? 0 : c->cap_stage;
     p.seg_counts = c->d_segc;
   }
 
@@ -996,7 +998,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
-                        cap, out_kind, host_out, false);
+                        cap, out_kind, host_out, false, count_only);
     return AP_OK;
   }
   fn<<<dim3(unsigned(grid)), dim3(wpc * 32), sh.smem, st>>>(p);
@@ -1012,11 +1014,11 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
-                        cap, out_kind, host_out, false);
+                        cap, out_kind, host_out, false, count_only);
     const size_t nrec = c->h_cursor[0];
     const size_t total = c->h_cursor[1];
     if (nrec != total) return fail(AP_CUDA, "threshold bookkeeping mismatch (%zu staged vs %zu counted)", nrec, total);
-    if (nrec > c->cap_stage) {
+    if (nrec > c->cap_stage && !count_only) {
       // staging overflowed: grow to the exact size and recompute (rare)
       if ((rc = grow(&c->d_stage, &c->cap_stage, nrec))) return rc;
       p.stage = c->d_stage;
@@ -1027,7 +1029,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       CK(cudaGetLastError());
       c->last_launches += 1;
     }
-    c->list.nrec = nrec;
+    c->list.nrec = count_only ? 0 : nrec;
     c->list.seg_stride = p.seg_stride;
     c->list.S = uint32_t(S);
     c->list.S2 = p.S2;
@@ -1042,7 +1044,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     CK(cudaStreamSynchronize(st));
     if (spec_failed())
       return run_device(c, d_x, mx, d_y, n, cfg, nrows, row_global0, dense, d_out, st, nrec_out, total_out,
-                        cap, out_kind, host_out, false);
+                        cap, out_kind, host_out, false, count_only);
   }
   return AP_OK;
 }
@@ -1270,7 +1272,8 @@ int ap_ctx_plot_threshold_device(ap_ctx* c, const uint8_t* d_x, size_t m, const 
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const size_t off = rb * cfg->step_h;
   size_t nrec = 0, total = 0;
-  rc = run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, false, nullptr, st, &nrec, &total, cap);
+  rc = run_device(c, d_x + off, m - off, d_y, n, cfg, re - rb, rb, false, nullptr, st, &nrec, &total, cap, 0, nullptr,
+                  true, cap == 0);
   if (rc) return rc;
   if ((rc = place_list(c, st, d_rows, d_cols, d_halves, nullptr, nullptr, cap))) return rc;
   CK(cudaStreamSynchronize(st));
@@ -1441,7 +1444,8 @@ int host_list(const uint8_t* x, size_t m, const uint8_t* y, size_t n, const ap_c
     size_t mx = 0, nrec = 0, total = 0;
     int q;
     if ((q = upload_shard(c, s, x, y, n, cfg, st, &mx))) return q;
-    if ((q = run_device(c, c->d_x, mx, c->d_y, n, cfg, nrows, s.r0, false, nullptr, st, &nrec, &total, 0)))
+    if ((q = run_device(c, c->d_x, mx, c->d_y, n, cfg, nrows, s.r0, false, nullptr, st, &nrec, &total, 0, 0, nullptr,
+                        true, cap_any == 0)))
       return q;
     s.total = total;
     s.kept = std::min(total, cap_any);

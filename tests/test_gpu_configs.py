@@ -116,3 +116,39 @@ def test_sampled_rows_vs_reference(name):
         assert_list_matches(lst, g, rb, re, c.t_half, name)
         checked += int(np.count_nonzero(g >= c.t_half))
     assert checked > 0
+
+
+def test_c4_count_only_beyond_2_pow_32():
+    """A count-only query (cap = 0) with a threshold below every score on the full C4 plot: the
+    count is rows * cols = 262081^2 = 68,686,450,561 > 2^32, exact through the 64-bit scan, and no
+    list is staged (a uint32 scan would wrap).  Through the device API and the host API
+    (which then reports AP_CAPACITY with the exact count)."""
+    import ctypes
+
+    import torch
+
+    from paper_0909_2000_b200 import _native
+    c = datagen.CONFIGS["C4"]
+    x, y = datagen.make_inputs("C4")
+    rows, cols = (x.size - c.w) // c.h + 1, y.size - c.w + 1
+    L = _native.lib()
+    cc = ap._cfg(cfg(c, -100))
+    count = ctypes.c_uint64()
+    ctx = ctypes.c_void_p()
+    assert L.ap_ctx_create(0, ctypes.byref(ctx)) == 0
+    try:
+        dx, dy = torch.from_numpy(x.copy()).cuda(), torch.from_numpy(y.copy()).cuda()
+        rc = L.ap_ctx_plot_threshold_device(ctx, dx.data_ptr(), x.size, dy.data_ptr(), y.size, ctypes.byref(cc),
+                                            ctypes.byref(count), None, None, None, 0, None)
+        assert rc == _native.AP_CAPACITY and count.value == rows * cols > 2 ** 32
+    finally:
+        L.ap_ctx_destroy(ctx)
+    count2 = ctypes.c_uint64()
+    rc = L.ap_plot_threshold(x.ctypes.data, x.size, y.ctypes.data, y.size, ctypes.byref(cc), ctypes.byref(count2),
+                             None, None, None, 0)
+    assert rc == _native.AP_CAPACITY and count2.value == rows * cols
+    # and the config's own threshold, count-only, equals the length of its list
+    cc = ap._cfg(cfg(c, c.t_half))
+    rc = L.ap_plot_threshold(x.ctypes.data, x.size, y.ctypes.data, y.size, ctypes.byref(cc), ctypes.byref(count2),
+                             None, None, None, 0)
+    assert rc == _native.AP_CAPACITY and count2.value == ap.plot_threshold_arrays(x, y, cfg(c), c.t_half)[0].size
