@@ -559,10 +559,17 @@ def main():
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.impl == "engine" and args.dist_backend == "nccl":
+            # communicator set-up lines (rank, nRanks) on stderr, so a scaling run shows its ranks
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group("gloo")
+    if world > 1:
+        import torch.distributed as dist
+        log(f"[bench] rank {rank} of {world}: process group backend {dist.get_backend()}, "
+            f"world size {dist.get_world_size()}, local rank {local_rank}")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:
