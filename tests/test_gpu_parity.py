@@ -836,3 +836,38 @@ def test_large_window_packed_rebases_over_long_y():
         rc, want, err = ol.ref_compute_plot(x, y, w, 1, r, ol.SEA16, 16)
         assert rc == 0, err
         assert np.array_equal(ap.plot_dense_i32(x, y, cfg(w, 1, r)), want), (w, r)
+
+
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_multi_shard_capacity_and_cells(ndev, monkeypatch):
+    """Several shard devices (one GPU standing in): a fixed capacity that ends inside the second
+    shard's list gets exactly the first cap cells of the global row-major list, the ap_cell form
+    and the int32 dense form agree with one device, and a row range crossing shards too."""
+    import ctypes
+
+    from paper_0909_2000_b200 import _native
+    monkeypatch.setenv("AP_SHARDS_PER_DEVICE", str(ndev))
+    rng = np.random.default_rng(900 + ndev)
+    x = rng.integers(1, 5, 1200).astype(np.uint8)
+    y = np.concatenate([x[100:900], rng.integers(1, 5, 400)]).astype(np.uint8)
+    w, h, r = 40, 1, 2
+    rc, want = ol.plot_rows(x, y, w, h, r)
+    t = int(np.quantile(want, 0.97))
+    er, ec = np.nonzero(want >= t)
+    c = ap._cfg(cfg(w, h, r, t, n_devices=ndev))
+    L = _native.lib()
+    cap = int(er.size * 0.6)            # ends inside a later shard's part of the list
+    rr, cc, hh = (np.zeros(cap, dt) for dt in (np.uint32, np.uint32, np.uint16))
+    count = ctypes.c_uint64()
+    assert L.ap_plot_threshold(x.ctypes.data, x.size, y.ctypes.data, y.size, ctypes.byref(c), ctypes.byref(count),
+                               rr.ctypes.data, cc.ctypes.data, hh.ctypes.data, cap) == _native.AP_CAPACITY
+    assert count.value == er.size
+    assert np.array_equal(rr, er[:cap]) and np.array_equal(cc, ec[:cap])
+    assert np.array_equal(hh.astype(np.int32), want[er[:cap], ec[:cap]])
+    cells = ap.plot_threshold_cells(x, y, cfg(w, h, r, n_devices=ndev), t)
+    assert [q.row for q in cells] == er.tolist() and [q.score_half for q in cells] == want[er, ec].tolist()
+    dense = ap.plot_dense_i32(x, y, cfg(w, h, r, n_devices=ndev))
+    assert np.array_equal(dense, want)
+    part = ap.plot_threshold_arrays(x, y, cfg(w, h, r, n_devices=ndev), t, row_begin=300, row_end=900)
+    sel = (er >= 300) & (er < 900)
+    assert np.array_equal(part[0], er[sel]) and np.array_equal(part[1], ec[sel])
