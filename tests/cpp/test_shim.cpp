@@ -212,6 +212,21 @@ int main() {
       CHECK(d.str() == pgm);
     }
   }
+  {  // large windows: sea16 mode up to w*r = 65534 (model.cpp:57-59); LCS scores past 16 bits
+    std::mt19937 rng(9090);
+    const std::vector<std::uint8_t> xs = random_codes(rng, 32800, 4);
+    const Sequence x("x", xs), y("y", xs);
+    PlotConfig cfg;
+    cfg.mode = Mode::sea16; cfg.window_w = 32800; cfg.step_h = 1; cfg.blowup_r = 1;
+    const PlotGrid g = compute_plot(x, y, cfg);            // one cell: the LCS of a string with itself
+    CHECK(g.rows == 1 && g.cols == 1 && g.at(0, 0) == 2 * 32800);
+    const auto cells = compute_plot_threshold(x, y, cfg, 65000);
+    CHECK(cells.size() == 1 && cells[0].score_half == 65600);
+    cfg.window_w = 32767; cfg.blowup_r = 2;                // the alignment-score bound w*r = 65534
+    CHECK(compute_plot(x, y, cfg).at(0, 0) == 2 * 32767);
+    cfg.window_w = 32768;
+    CHECK_THROWS_AS(compute_plot(x, y, cfg), ConfigError);
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
   return failures;
 }

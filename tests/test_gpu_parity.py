@@ -871,3 +871,17 @@ def test_multi_shard_capacity_and_cells(ndev, monkeypatch):
     part = ap.plot_threshold_arrays(x, y, cfg(w, h, r, n_devices=ndev), t, row_begin=300, row_end=900)
     sel = (er >= 300) & (er < 900)
     assert np.array_equal(part[0], er[sel]) and np.array_equal(part[1], ec[sel])
+
+
+def test_empty_row_ranges():
+    """row_begin == row_end (and a range past the last row): no device work, an empty dense block,
+    a zero count with one allocation callback of 0, for the packed and the large-window paths."""
+    rng = np.random.default_rng(12)
+    x = rng.integers(1, 5, 3000).astype(np.uint8)
+    y = rng.integers(1, 5, 3200).astype(np.uint8)
+    for w, r in ((40, 1), (30, 2), (1500, 1)):
+        rows = x.size - w + 1
+        for rb, re in ((5, 5), (rows, rows + 10)):
+            assert ap.plot_dense_u16(x, y, cfg(w, 1, r), rb, re).shape[0] == 0
+            got = ap.plot_threshold_arrays(x, y, cfg(w, 1, r), -10, row_begin=rb, row_end=re)
+            assert all(a.size == 0 for a in got), (w, r, rb, re)
