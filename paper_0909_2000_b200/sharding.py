@@ -75,6 +75,39 @@ def gather_counts(local_count: int, group=None) -> Tuple[int, int]:
     return sum(counts[:rank]), sum(counts)
 
 
+def gather_list_to_root(rows: np.ndarray, cols: np.ndarray, halves: np.ndarray, root: int = 0, group=None):
+    """Concatenate every rank's row-major part of a thresholded list on `root`, in rank (= row)
+    order: apply_threshold's whole list (scoring.cpp:30-39) where the caller wants it in one place.
+
+    One all_gather of the counts, then each rank's (row, col, half) triples padded to the longest
+    part and all_gathered as one int64 tensor (NCCL over NVLink on GPUs, device-resident when the
+    backend is NCCL; gloo in CPU tests).  Returns (rows, cols, halves) on root and None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    n = int(rows.size)
+    cnt = torch.tensor([n], dtype=torch.int64, device=dev)
+    cnts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    counts = [int(v.item()) for v in cnts]
+    width = max(max(counts), 1)
+    mine = torch.zeros((3, width), dtype=torch.int64, device=dev)
+    if n:
+        mine[0, :n] = torch.from_numpy(rows.astype(np.int64)).to(dev)
+        mine[1, :n] = torch.from_numpy(cols.astype(np.int64)).to(dev)
+        mine[2, :n] = torch.from_numpy(halves.astype(np.int16).astype(np.int64)).to(dev)
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    if rank != root:
+        return None
+    full = torch.cat([p_[:, :c] for p_, c in zip(parts, counts)], dim=1).cpu().numpy()
+    return full[0].astype(np.uint32), full[1].astype(np.uint32), full[2].astype(np.int32)
+
+
 def run_sharded_threshold(x: np.ndarray, y: np.ndarray, w: int, h: int, rank: int, world: int,
                           compute: Callable[[np.ndarray, np.ndarray, int], Tuple[np.ndarray, np.ndarray, np.ndarray]],
                           group=None):

@@ -14,7 +14,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle_lib as ol
-from paper_0909_2000_b200.sharding import plan_row_shards, run_sharded_dense, run_sharded_threshold, shard_x
+from paper_0909_2000_b200.sharding import (gather_list_to_root, plan_row_shards, run_sharded_dense,
+                                           run_sharded_threshold, shard_x)
 
 
 def test_plan_covers_rows_once_with_halo():
@@ -54,7 +55,8 @@ def _worker(rank, world, port, x, y, w, h, r, t, q):
 
         off, total, rr, cc, hh = run_sharded_threshold(x, y, w, h, rank, world, compute_thr)
         r0, block = run_sharded_dense(x, y, w, h, rank, world, compute_dense)
-        q.put((rank, off, total, rr, cc, hh, r0, block))
+        whole = gather_list_to_root(rr, cc, hh, root=0)
+        q.put((rank, off, total, rr, cc, hh, r0, block, whole))
     finally:
         dist.destroy_process_group()
 
@@ -87,7 +89,7 @@ def test_gloo_matches_single_process(w, h, r, world):
     out_h = np.zeros(total, np.uint16)
     shards = plan_row_shards(x.size, w, h, world)
     expect_off = 0
-    for rank, off, _, rr, cc, hh, r0, block in res:
+    for rank, off, _, rr, cc, hh, r0, block, whole in res:
         assert off == expect_off   # exclusive prefix of the gathered counts, in rank (= row) order
         expect_off += rr.size
         s = shards[rank]
@@ -95,6 +97,10 @@ def test_gloo_matches_single_process(w, h, r, world):
         assert rr.size == int(np.count_nonzero(full[s.row_begin:s.row_end] >= t))
         out_r[off:off + rr.size], out_c[off:off + cc.size], out_h[off:off + hh.size] = rr, cc, hh
     assert np.array_equal(out_r, er) and np.array_equal(out_c, ec) and np.array_equal(out_h, full[er, ec])
+    # the whole list gathered on rank 0 (None elsewhere) is apply_threshold's row-major list
+    gr, gc, gh = res[0][8]
+    assert np.array_equal(gr, er) and np.array_equal(gc, ec) and np.array_equal(gh, full[er, ec])
+    assert all(v[8] is None for v in res[1:])
     dense = np.concatenate([v[7] for v in res], axis=0)
     assert np.array_equal(dense, full)
     assert [v[6] for v in res] == [s.row_begin for s in plan_row_shards(x.size, w, h, world)]
