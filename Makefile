@@ -7,8 +7,8 @@ PKG := paper_0909_2000_b200
 CSRC := $(PKG)/csrc
 BUILD ?= build
 LIB ?= $(PKG)/libalignplot_b200.so
-OBJS := $(BUILD)/ap_capi.o $(BUILD)/ap_inst_l4.o $(BUILD)/ap_inst_l8.o $(BUILD)/ap_inst_l16.o $(BUILD)/ap_inst_l32.o $(BUILD)/ap_inst_r2.o $(BUILD)/ap_inst_r2hf.o $(BUILD)/ap_inst_ghf_a.o $(BUILD)/ap_inst_ghf_b.o $(BUILD)/ap_inst_ghf_c.o
-HDRS := $(CSRC)/ap_kernels.cuh $(CSRC)/ap_aux_kernels.cuh $(CSRC)/ap_wide_kernels.cuh include/alignplot_b200.h
+OBJS := $(BUILD)/ap_capi.o $(BUILD)/ap_inst_l4.o $(BUILD)/ap_inst_l8.o $(BUILD)/ap_inst_l16.o $(BUILD)/ap_inst_l32.o $(BUILD)/ap_inst_r2.o $(BUILD)/ap_inst_r2hf.o $(BUILD)/ap_inst_ghf_a.o $(BUILD)/ap_inst_ghf_b.o $(BUILD)/ap_inst_ghf_c.o $(BUILD)/ap_inst_dual_a.o $(BUILD)/ap_inst_dual_b.o
+HDRS := $(CSRC)/ap_kernels.cuh $(CSRC)/ap_aux_kernels.cuh $(CSRC)/ap_wide_kernels.cuh $(CSRC)/ap_dual_kernels.cuh include/alignplot_b200.h
 
 all: $(LIB) oracle
 
@@ -19,12 +19,13 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 $(BUILD):
-	mkdir -p $(BUILD)
+	mkdir -p $(BUILD) $(dir $(LIB))
 
 # experiment builds: make variant V=name FLAGS="-DFOO" -> tools/exp/name/libalignplot_b200.so
 # (load with AP_LIB_PATH=tools/exp/name/libalignplot_b200.so)
 variant:
-	$(MAKE) BUILD=tools/exp/$(V)/obj LIB=tools/exp/$(V)/libalignplot_b200.so EXTRA_NVFLAGS="$(FLAGS)" \
+	mkdir -p tools/exp/$(V)
+	$(MAKE) BUILD=/tmp/apbuild/$(V) LIB=tools/exp/$(V)/libalignplot_b200.so EXTRA_NVFLAGS="$(FLAGS)" \
 	  tools/exp/$(V)/libalignplot_b200.so
 
 oracle:

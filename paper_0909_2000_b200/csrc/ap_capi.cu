@@ -28,6 +28,7 @@
 #include "ap_aux_kernels.cuh"
 #include "ap_kernels.cuh"
 #include "ap_wide_kernels.cuh"
+#include "ap_dual_kernels.cuh"
 
 namespace {
 
@@ -86,6 +87,7 @@ struct Shape {
   bool r2 = false;   // r = 2 specialised kernel (comb2_kernel); R = 2*RR then
   bool xm = false;   // masks computed in registers (no table)
   bool hf = false;   // fp16 keys: one cell op per row (r = 2: a mismatch min; generic: V' of one row in 4) on the FMA pipe
+  bool dual = false; // two strip pairs per lane group sharing the mask table (combd_kernel: r = 1, h = 1, W = L*R)
   uint32_t ring = 0;
   size_t smem = 0;
   int warps_per_sm = 0;
@@ -94,11 +96,34 @@ struct Shape {
 // Cost per strip pair and column: L lanes x (3 ops per row pair [6 with computed
 // masks] + ~14 per-step overhead) + ~25 extraction ops, scaled up when fewer than
 // 16 warps per SM fit (registers from the compiled kernel, table in shared memory).
-bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
-  // tuning override: AP_SHAPE="L,R,K[,xm[,hf]]" (hf default: the automatic choice)
+// Dual-pair shapes (combd_kernel, ap_dual_kernels.cuh), in order of preference per window:
+// usable when W == L*R exactly (LCS plots with h = 1).
+constexpr ShapeDef kDualShapes[] = {
+    {4, 32, 1}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {8, 8, 2}, {4, 16, 2},
+    {4, 32, 2}, {8, 32, 1}, {8, 16, 1}, {16, 16, 2}, {8, 8, 1},
+};
+
+bool dual_shape_fits(uint32_t W, uint32_t sigma, bool dense, int l, int r, int k, int hf, Shape* out) {
+  if (uint32_t(l * r) != W) return false;
+  if (hf < 0) hf = ghf_ok(W, l, k);
+  if (hf && !ghf_ok(W, l, k)) return false;
+  if (!apk::pick_dual(l, r, k, dense, hf)) return false;
+  const uint32_t ring = apk::ring_slots(W, apk::kChunk, l);
+  const size_t smem = apk::combd_smem_per_warp(l, r, k, sigma, ring);
+  if (smem > kSmemPerSm / 4) return false;   // keep at least 4 warps per SM
+  out->L = l; out->R = r; out->K = k; out->xm = false; out->hf = hf; out->dual = true; out->r2 = false;
+  out->ring = ring;
+  out->smem = smem * apk::kWarpsPerCta;   // shapes are recorded for 4-warp CTAs (rescaled by the plan)
+  out->warps_per_sm = 0;
+  return true;
+}
+
+bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out, bool dual_ok = false) {
+  // tuning override: AP_SHAPE="L,R,K[,xm[,hf[,dual]]]" (hf default: the automatic choice)
   if (const char* env = std::getenv("AP_SHAPE")) {
-    int l = 0, r = 0, k = 0, xm = 0, hf = -1;
-    const int nf = std::sscanf(env, "%d,%d,%d,%d,%d", &l, &r, &k, &xm, &hf);
+    int l = 0, r = 0, k = 0, xm = 0, hf = -1, dual = 0;
+    const int nf = std::sscanf(env, "%d,%d,%d,%d,%d,%d", &l, &r, &k, &xm, &hf, &dual);
+    if (nf >= 6 && dual && dual_ok && !xm && dual_shape_fits(W, sigma, dense, l, r, k, hf, out)) return true;
     if (hf < 0) hf = !xm && ghf_ok(W, l, k) && pick_kernel(l, r, k, dense, false, true);
     if (nf >= 3 && (!hf || ghf_ok(W, l, k)) && pick_kernel(l, r, k, dense, xm, hf) && uint32_t(l * r) >= W) {
       const uint32_t ring = apk::ring_slots(W, apk::kChunk, l);
@@ -108,6 +133,11 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out) {
       return out->smem <= kSmemPerSm - 1024;
     }
   }
+  if (dual_ok && !std::getenv("AP_NO_DUAL") && !std::getenv("AP_SHAPE")) {
+    for (const ShapeDef& d : kDualShapes)
+      if (dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out)) return true;
+  }
+  out->dual = false;
   double best = 1e30;
   for (int xm = 0; xm < 2; ++xm) {
     for (const ShapeDef& d : kShapes) {
@@ -676,7 +706,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   // code stays above every real code) -- and let the comb kernel verify on the device: if y
   // has more codes, every warp exits and flags the launch, and the call re-runs synchronously.
   // This removes the host round trip between the alphabet pass and the comb (C1: ~20 us).
-  const bool overrides = std::getenv("AP_SHAPE") || std::getenv("AP_SHAPE2") || std::getenv("AP_NO_R2");
+  const bool overrides = std::getenv("AP_SHAPE") || std::getenv("AP_SHAPE2") || std::getenv("AP_NO_R2") ||
+                         std::getenv("AP_NO_DUAL");
   const uint64_t skey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(out_kind) << 2) | (dense ? 1 : 0);
   const auto spec_hit = c->last_sigma.find(skey);
   const bool wide = W > AP_PACKED_WINDOW;   // the large-window path plans nothing by sigma
@@ -746,17 +777,19 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   // launch plan (shape choice, function attributes, occupancy), cached per context;
   // tuning overrides (AP_SHAPE, AP_SHAPE2, AP_NO_R2) bypass the cache
-  const uint64_t pkey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(sigma_y) << 2) | (dense ? 1 : 0);
+  const uint64_t pkey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(sigma_y) << 2) | (h == 1 ? 2 : 0) |
+                        (dense ? 1 : 0);
   LaunchPlan plan;
   auto hit = overrides ? c->plans.end() : c->plans.find(pkey);
   if (hit != c->plans.end()) {
     plan = hit->second;
   } else {
     plan.spec = r == 2 && choose_shape2(w, sigma_y, dense, &plan.sh);
-    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh))
+    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh, r == 1 && h == 1))
       return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                   sigma, W);
     plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf)
+              : plan.sh.dual ? apk::pick_dual(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.hf)
                         : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm, plan.sh.hf);
     if (!plan.fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", plan.sh.L, plan.sh.R);
     // warps per CTA, as compiled into the kernel (ap_kernels.cuh kGenericWpc / r2_wpc)
@@ -774,8 +807,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     std::snprintf(c->last_kernel, sizeof(c->last_kernel), "comb2<%d,%d,%d,%s>", sh.L, sh.R / 2, sh.K,
                   sh.hf ? "fp16" : "int");
   else
-    std::snprintf(c->last_kernel, sizeof(c->last_kernel), "comb<%d,%d,%d,%s,%s>", sh.L, sh.R, sh.K,
-                  sh.xm ? "computed" : "table", sh.hf ? "fp16" : "int");
+    std::snprintf(c->last_kernel, sizeof(c->last_kernel), "%s<%d,%d,%d,%s,%s>", sh.dual ? "combd" : "comb", sh.L,
+                  sh.R, sh.K, sh.xm ? "computed" : "table", sh.hf ? "fp16" : "int");
   // the dynamic-smem limit is a per-function attribute and other plans may have
   // lowered it since this plan was cached
   CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(plan.fn),
@@ -810,7 +843,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   // column segments: enough independent (strip pair, segment) tasks for ~4
   // waves, each segment at least 4 windows wide to bound the W-1 overlap.
-  const int G = 32 / sh.L;
+  const int G = 32 / sh.L * (sh.dual ? 2 : 1);   // strip pairs per warp
   const size_t npairs = (nrows + 1) / 2;
   const size_t ngroups = (npairs + G - 1) / G;
   const size_t out_cols_eff = (N - W) + 1;  // window starts in effective columns (stride 1)
@@ -836,6 +869,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.ycol = c->d_ycol;
   p.ycol_zero = spec ? nullptr : c->d_ycol + ytot;
   p.rows = uint32_t(nrows);
+  p.xlen = uint32_t(mx);
   p.h = h;
   p.w = w;
   p.r = r;
@@ -953,6 +987,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
       cudaStream_t sk = (!d2h_bound && (k & 1)) ? c->stream_b : st;
       apk::CombParams pk = p;
       pk.xcode = c->d_xcode + r0 * h;
+      pk.xlen = uint32_t(mx - r0 * h);
       pk.rows = uint32_t(r1 - r0);
       pk.row_global0 = uint32_t(row_global0 + r0);
       pk.out = p.out + (out_kind == 0 ? r0 * cols : 0);

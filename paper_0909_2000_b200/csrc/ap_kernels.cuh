@@ -72,6 +72,7 @@ struct CombParams {
   const uint32_t* ycol;   // generic kernel: code * ycol_mult per effective column (+256 pad), 16-B aligned
   const uint32_t* ycol_zero;  // as many zero words (the column words seen by lanes j != 0)
   uint32_t rows;          // grid rows in this launch
+  uint32_t xlen;          // x codes readable from xcode (dual-pair kernel: words of rows past this launch's own)
   uint32_t h, w, r, W, N; // step, window, blowup, blown window, effective y length
   uint32_t sigma;         // table codes (incl. the sentinel code when r = 2)
   uint32_t sent_code;     // code of the $ sentinel (r = 2)
@@ -195,6 +196,9 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+#ifndef AP_ABL_LDS
+#define AP_ABL_LDS 1   // timing ablation only (wrong results when > 1): one table load per AP_ABL_LDS quads
+#endif
 #ifndef AP_FMAMIN_RR
 #define AP_FMAMIN_RR 4   // r = 2 kernels with RR >= this compute one mismatch min with IMADs (C4: -1.3%)
 #endif
@@ -820,7 +824,9 @@ comb_kernel(const CombParams p) {
             for (int b = 0; b < K; ++b)
 #pragma unroll
               for (int qq = 0; qq < QB; ++qq)
-                nfq[b * QB + qq] = lds128(madhi(cd[b], tblmul, tlb) + (b * QB + qq) * L * 16);
+                nfq[b * QB + qq] = (b * QB + qq) % AP_ABL_LDS == 0
+                                       ? lds128(madhi(cd[b], tblmul, tlb) + (b * QB + qq) * L * 16)
+                                       : nfq[(b * QB + qq) - (b * QB + qq) % AP_ABL_LDS];
           }
           // seaweeds entering each band
           uint32_t tin[K];
