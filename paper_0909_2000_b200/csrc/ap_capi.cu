@@ -707,7 +707,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   // has more codes, every warp exits and flags the launch, and the call re-runs synchronously.
   // This removes the host round trip between the alphabet pass and the comb (C1: ~20 us).
   const bool overrides = std::getenv("AP_SHAPE") || std::getenv("AP_SHAPE2") || std::getenv("AP_NO_R2") ||
-                         std::getenv("AP_NO_DUAL");
+                         std::getenv("AP_NO_DUAL") || std::getenv("AP_DUAL");
   const uint64_t skey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(out_kind) << 2) | (dense ? 1 : 0);
   const auto spec_hit = c->last_sigma.find(skey);
   const bool wide = W > AP_PACKED_WINDOW;   // the large-window path plans nothing by sigma
@@ -777,7 +777,14 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
 
   // launch plan (shape choice, function attributes, occupancy), cached per context;
   // tuning overrides (AP_SHAPE, AP_SHAPE2, AP_NO_R2) bypass the cache
-  const uint64_t pkey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(sigma_y) << 2) | (h == 1 ? 2 : 0) |
+  // the dual-pair kernel (two strip pairs per lane group) needs LCS strips one character apart
+  // and enough (pair, segment) tasks to fill the GPU with half as many pair groups (C1 does not:
+  // 0.049 -> 0.058 ms); AP_DUAL=1 forces it for eligible plots
+  const size_t max_nseg = std::max<size_t>(1, (N - W + 1) / std::max<size_t>(4 * W, 256));
+  const char* dual_env = std::getenv("AP_DUAL");
+  const bool dual_ok = r == 1 && h == 1 &&
+                       (dual_env ? std::atoi(dual_env) != 0 : ((nrows + 1) / 2) * max_nseg >= size_t(16) * 12 * c->sms);
+  const uint64_t pkey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(sigma_y) << 2) | (dual_ok ? 2 : 0) |
                         (dense ? 1 : 0);
   LaunchPlan plan;
   auto hit = overrides ? c->plans.end() : c->plans.find(pkey);
@@ -785,7 +792,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
     plan = hit->second;
   } else {
     plan.spec = r == 2 && choose_shape2(w, sigma_y, dense, &plan.sh);
-    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh, r == 1 && h == 1))
+    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh, dual_ok))
       return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                   sigma, W);
     plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf)

@@ -208,6 +208,114 @@ def test_forced_generic_shapes(shape, monkeypatch):
         assert np.array_equal(gpu_grid(x, y, w, 2, r), want), (shape, r)
 
 
+DUAL_SHAPES = ["4,32,1", "4,32,2", "8,32,1", "8,32,2", "8,16,1", "8,16,2", "16,16,1", "16,16,2", "8,8,1", "8,8,2",
+               "4,16,2"]
+
+
+def last_kernel_name(x, y, w, h, r):
+    """Name of the comb kernel a dense device-API plot of (x, y) launches (ap_ctx_last_kernel)."""
+    import ctypes
+
+    import torch
+
+    from paper_0909_2000_b200 import _native
+    L = _native.lib()
+    ctx = ctypes.c_void_p()
+    assert L.ap_ctx_create(0, ctypes.byref(ctx)) == 0
+    c = _native.ApConfig(window_w=w, step_h=h, blowup_r=r, has_threshold=0, threshold_half=0, n_devices=1,
+                         row_begin=0, row_end=0)
+    dx, dy = torch.from_numpy(x.copy()).cuda(), torch.from_numpy(y.copy()).cuda()
+    rows, cols = (x.size - w) // h + 1, y.size - w + 1
+    out = torch.empty(rows * cols, dtype=torch.int16, device="cuda")
+    rc = L.ap_ctx_plot_dense_device(ctx, dx.data_ptr(), x.size, dy.data_ptr(), y.size, ctypes.byref(c),
+                                    out.data_ptr(), None)
+    assert rc == 0, _native.last_error()
+    name = (L.ap_ctx_last_kernel(ctx) or b"").decode()
+    L.ap_ctx_destroy(ctx)
+    return name, out.cpu().numpy().astype(np.uint16).astype(np.int32).reshape(rows, cols)
+
+
+@pytest.mark.parametrize("shape", [s + ",0,0,1" for s in DUAL_SHAPES] + [s + ",0,1,1" for s in DUAL_SHAPES])
+def test_forced_dual_shapes(shape, monkeypatch):
+    """Every instantiated dual-pair shape (two strip pairs per lane group sharing one mask table,
+    ap_dual_kernels.cuh), integer and fp16 keys, dense and thresholded, for row counts of every
+    residue mod 4 (a group holds grid rows 4g .. 4g+3)."""
+    monkeypatch.setenv("AP_SHAPE", shape)
+    monkeypatch.setenv("AP_DUAL", "1")
+    L, R, K = map(int, shape.split(",")[:3])
+    w = L * R
+    rng = np.random.default_rng(sum(map(ord, shape)))
+    for extra in range(4):
+        x = rng.integers(1, 5, w + 70 + extra).astype(np.uint8)
+        y = np.concatenate([rng.integers(1, 5, 300), x[5:w + 40], rng.integers(1, 5, 400)]).astype(np.uint8)
+        if extra == 0:
+            name, grid = last_kernel_name(x, y, w, 1, 1)
+            assert name.startswith("combd<%d,%d,%d," % (L, R, K)), name
+        rc, want = ol.plot_rows(x, y, w, 1, 1)
+        assert rc == 0
+        assert np.array_equal(gpu_grid(x, y, w, 1, 1), want), (shape, extra)
+        t = int(np.quantile(want, 0.97))
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 1), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (shape, extra)
+
+
+@pytest.mark.parametrize("w,sigma", [(64, 4), (128, 4), (256, 4), (128, 20), (256, 2)])
+def test_dual_kernel_long_y_and_row_ranges(w, sigma, monkeypatch):
+    """The dual-pair kernel as the default plan picks it (AP_DUAL=1 lifts the problem-size gate):
+    a y long enough for interior chunks and fp16-key rebases with planted homology, odd row
+    ranges, bytes of x absent from y, dense and thresholded."""
+    monkeypatch.setenv("AP_DUAL", "1")
+    rng = np.random.default_rng(w + sigma)
+    x = rng.integers(1, sigma + 1, w + 22).astype(np.uint8)
+    x[w // 2] = 200   # absent from y
+    parts = []
+    while sum(p.size for p in parts) < 40000:
+        parts.append(rng.integers(1, sigma + 1, int(rng.integers(50, 2500))).astype(np.uint8))
+        blk = x[int(rng.integers(0, 20)):][:w + 10].copy()
+        blk[blk == 200] = 1
+        flip = rng.random(blk.size) < 0.06
+        blk[flip] = rng.integers(1, sigma + 1, int(flip.sum()))
+        parts.append(blk)
+    y = np.concatenate(parts)
+    name, grid = last_kernel_name(x, y, w, 1, 1)
+    assert name.startswith("combd<"), name
+    rc, want = ol.plot_rows(x, y, w, 1, 1)
+    assert rc == 0 and np.array_equal(grid, want)
+    assert np.array_equal(gpu_grid(x, y, w, 1, 1), want)
+    for rb, re in ((1, 2), (3, 10), (5, 23), (22, 23)):
+        assert np.array_equal(gpu_grid(x, y, w, 1, 1, rb, re), want[rb:re]), (rb, re)
+    for t in (int(np.quantile(want, 0.999)), int(want.max())):
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 1), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), t
+
+
+def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
+    """Small plots keep the single-pair kernel (too few pair groups to fill the GPU), large ones
+    take the dual-pair kernel; the streamed host plot (row blocks whose mask words reach into
+    the next block's x characters) equals the one-launch device plot and the oracle."""
+    rng = np.random.default_rng(99)
+    x = rng.integers(1, 5, 2600).astype(np.uint8)
+    y = np.concatenate([x[300:1200], rng.integers(1, 5, 1500)]).astype(np.uint8)
+    name, _ = last_kernel_name(x[:400], y[:600], 64, 1, 1)
+    assert name.startswith("comb<"), name
+    monkeypatch.setenv("AP_DUAL", "1")
+    name, grid = last_kernel_name(x, y, 64, 1, 1)
+    assert name.startswith("combd<"), name
+    rc, want = ol.plot_rows(x, y, 64, 1, 1)
+    assert rc == 0 and np.array_equal(grid, want)
+    assert np.array_equal(gpu_grid(x, y, 64, 1, 1), want)
+    monkeypatch.delenv("AP_DUAL")
+    big_x = rng.integers(1, 5, 70000).astype(np.uint8)
+    big_y = rng.integers(1, 5, 9000).astype(np.uint8)
+    name, grid = last_kernel_name(big_x, big_y, 64, 1, 1)
+    assert name.startswith("combd<"), name
+    for rb in (0, 33333, 69935):
+        rc, wr = ol.plot_rows(big_x, big_y, 64, 1, 1, rb, rb + 2)
+        assert np.array_equal(grid[rb:rb + 2], wr), rb
+
+
 R2_SHAPES = ["4,25,5", "4,25,1", "10,10,2", "10,10,1", "5,20,4", "5,20,1", "8,8,2", "8,8,4", "16,8,4",
              "32,8,4", "8,16,4", "16,16,4", "32,16,4", "16,4,2", "32,4,2", "16,10,2", "8,20,4", "32,5,1",
              "32,4,1", "16,4,1"]
