@@ -10,10 +10,11 @@ namespace apk {
 // K1: effective y code stream (fused $-interleave, scoring.cpp:5-17):
 // ycode[c] = r == 2 ? (c odd ? map[y[c/2]] : sent) : map[y[c]]; pad with 0.
 // With ycol != nullptr also the generic kernel's column words ycol[c] =
-// ycode[c] * 0x10001 followed by `total` zero words (what lanes j != 0 read).
+// ycode[c] * ycol_mult followed by `total` zero words (what lanes j != 0 read); ycol_mult is
+// 0x10001 (the code in both halves) or, for the dual-pair kernel, the table's byte stride per code.
 __global__ void ycode_kernel(const uint8_t* __restrict__ y, size_t n, uint32_t r, uint32_t sent,
                              const uint8_t* __restrict__ map, uint8_t* __restrict__ ycode,
-                             size_t total, uint32_t* __restrict__ ycol) {
+                             size_t total, uint32_t* __restrict__ ycol, uint32_t ycol_mult = 0x00010001u) {
   for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < total;
        c += size_t(gridDim.x) * blockDim.x) {
     const size_t N = n * r;
@@ -21,7 +22,7 @@ __global__ void ycode_kernel(const uint8_t* __restrict__ y, size_t n, uint32_t r
     if (c < N) v = (r == 2) ? ((c & 1) ? map[y[c >> 1]] : uint8_t(sent)) : map[y[c]];
     ycode[c] = v;
     if (ycol) {
-      ycol[c] = uint32_t(v) * 0x00010001u;
+      ycol[c] = uint32_t(v) * ycol_mult;
       ycol[total + c] = 0u;
     }
   }
@@ -67,7 +68,8 @@ __global__ void alphabet_kernel(const uint8_t* __restrict__ y, size_t n, uint8_t
 __global__ void codes_small_kernel(const uint8_t* __restrict__ x, size_t m, const uint8_t* __restrict__ y,
                                    size_t n, uint32_t r, uint32_t sent, uint8_t* __restrict__ map,
                                    uint32_t* __restrict__ small, uint8_t* __restrict__ xcode,
-                                   uint8_t* __restrict__ ycode, size_t total, uint32_t* __restrict__ ycol) {
+                                   uint8_t* __restrict__ ycode, size_t total, uint32_t* __restrict__ ycol,
+                                   uint32_t ycol_mult = 0x00010001u) {
   __shared__ uint32_t present[256];
   __shared__ uint32_t wsum[8];
   __shared__ uint8_t smap[256];
@@ -97,7 +99,7 @@ __global__ void codes_small_kernel(const uint8_t* __restrict__ x, size_t m, cons
     if (c < N) v = (r == 2) ? ((c & 1) ? smap[y[c >> 1]] : uint8_t(sent)) : smap[y[c]];
     ycode[c] = v;
     if (ycol) {
-      ycol[c] = uint32_t(v) * 0x00010001u;
+      ycol[c] = uint32_t(v) * ycol_mult;
       ycol[total + c] = 0u;
     }
   }

@@ -828,9 +828,11 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t ytot = (ylen + 256 + 31) / 32 * 32;
   if ((rc = grow(&c->d_ycode, &c->cap_ycode, ytot))) return rc;
   if (!spec && (rc = grow(&c->d_ycol, &c->cap_ycol, 2 * ytot))) return rc;   // ytot: multiple of 32
+  // column words: the code in both halves, or for the dual-pair kernel its table offset
+  const uint32_t ycol_mult = sh.dual ? uint32_t(sh.L * apk::dual_pj(sh.L, sh.R) * 16) : 0x00010001u;
   if (fused_codes) {
     apk::codes_small_kernel<<<1, 1024, 0, st>>>(d_x, mx, d_y, n, spec ? 1 : r, sent, c->d_map, c->d_small,
-                                                c->d_xcode, c->d_ycode, ytot, spec ? nullptr : c->d_ycol);
+                                                c->d_xcode, c->d_ycode, ytot, spec ? nullptr : c->d_ycol, ycol_mult);
     CK(cudaGetLastError());
     c->last_launches += 1;
   } else {
@@ -838,7 +840,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
                                                                                  c->d_xcode);
     CK(cudaGetLastError());
     apk::ycode_kernel<<<std::min<size_t>((ytot + 255) / 256, 4096), 256, 0, st>>>(
-        d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot, spec ? nullptr : c->d_ycol);
+        d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot, spec ? nullptr : c->d_ycol, ycol_mult);
     CK(cudaGetLastError());
     c->last_launches += 3;
   }

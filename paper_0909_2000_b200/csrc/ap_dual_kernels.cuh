@@ -13,7 +13,7 @@
 // x-window of the pair (4g, 4g+1) shifted by two characters, so its mask word
 // of strip row i is the first pair's word of row i + 2: a lane that holds rows
 // [jR, jR+R) of BOTH pairs reads R + 2 words (R/4 LDS.128 + one LDS.64 per
-// band) for 4R cells instead of 2R — 1.8x fewer table wavefronts per cell, four
+// band: the first half of the quad below it) for 4R cells instead of 2R — 1.8x fewer table wavefronts per cell, four
 // independent seaweed chains per lane (K = 2 bands x 2 pairs), and the per-step
 // overhead (shuffles, code feed, table addresses) shared by twice the cells.
 //
@@ -41,12 +41,11 @@ __host__ __device__ constexpr int dual_pj(int L, int R) {
   return L >= 8 ? (need | 1) : need + (6 - need % 4) % 4;
 }
 
-// Shared memory per warp (one-warp CTAs): the mask table [sigma][L][PJ] quads, the two extra
-// words per (code, band, lane), two bottom-key rings per group, one ok-flag ring per group.
+// Shared memory per warp (one-warp CTAs): the mask table [sigma][L][PJ] quads, two bottom-key
+// rings per group, one ok-flag ring per group.
 __host__ __device__ inline size_t combd_smem_per_warp(int L, int R, int K, uint32_t sigma, uint32_t ring) {
   const int G = 32 / L;
   const size_t bytes = size_t(16) * sigma * L * dual_pj(L, R)
-       + size_t(sigma) * K * 256
        + ((size_t(2) * G * ring_stride(L, kChunk) * 4 + 15) & ~size_t(15))
        + size_t(G) * ok_stride(ring);
   return (bytes + 15) & ~size_t(15);
@@ -87,8 +86,6 @@ combd_kernel(const CombParams p) {
   constexpr int QB = RB / 4;
   constexpr int VB = L * K;
   constexpr int PJ = dual_pj(L, R);
-  constexpr uint32_t kTblMul = uint32_t(L * PJ * 16) << 16;
-  constexpr uint32_t kExtMul = uint32_t(K * 256) << 16;
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
@@ -96,8 +93,7 @@ combd_kernel(const CombParams p) {
   const uint32_t j = lane % L;
   uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][L][PJ]
   const size_t tbytes = size_t(p.sigma) * L * PJ * 16;
-  uint2* tblx = reinterpret_cast<uint2*>(smem + tbytes);             // [sigma][K][32]
-  const size_t xbytes = size_t(p.sigma) * K * 256;
+  constexpr size_t xbytes = 0;
   constexpr int RSG = ring_stride(L, kChunk);
   uint32_t* ring0 = reinterpret_cast<uint32_t*>(smem + tbytes + xbytes) + g * RSG;
   uint32_t* ring1 = ring0 + G * RSG;
@@ -159,30 +155,11 @@ combd_kernel(const CombParams p) {
           tbl[(a * L + jj) * PJ + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
-#pragma unroll
-      for (int b = 0; b < K; ++b) {
-        uint32_t xc[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const uint32_t idx = r0 + j * R + (b + 1) * RB + k;
-          uint32_t cv = 0x1FFu;
-          if (idx < p.xlen) {
-            cv = p.xcode[idx];
-            if (cv == 0xFFu) cv = 0x1FFu;
-          }
-          xc[k] = cv;
-        }
-        for (uint32_t a = 0; a < p.sigma; ++a)
-          tblx[(a * K + b) * 32 + lane] =
-              make_uint2((xc[0] == a ? 0x00008000u : 0u) | (xc[1] == a ? 0x80000000u : 0u),
-                         (xc[1] == a ? 0x00008000u : 0u) | (xc[2] == a ? 0x80000000u : 0u));
-      }
       for (uint32_t k = j; k < p.ring; k += L) sts_u32(okb + 4 * k, 0u);
     }
     __syncwarp();
 
     const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + j * PJ + g));
-    const uint32_t txb = uint32_t(__cvta_generic_to_shared(tblx + lane));
     const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
     const uint32_t nz = j != 0 ? 1u : 0u;
     const uint32_t finc = j == 0 ? 0x00010001u : 0u;
@@ -198,19 +175,17 @@ combd_kernel(const CombParams p) {
     uint32_t fresh = j == 0 ? uint32_t(-kbase) * 0x00010001u : 0u;
     const uint32_t rebase_by = HF ? (kHfRebaseAt - kHfBase - 2 * kChunk - VB - p.W) : kRebaseBy;
     const uint32_t one = p.one;
-    const uint32_t tblmul = kTblMul * one;   // opaque: IMAD.HI (FMA pipe), not LEA.HI (ALU)
-    const uint32_t extmul = kExtMul * one;
     uint32_t run0 = 0u, run1 = 0u;
     uint32_t hits0 = 0u, hits1 = 0u, hits2 = 0u, hits3 = 0u;
 
-    uint4 qa = __ldg(yq), qb = __ldg(yq + 1), qc = __ldg(yq + 2), qd = __ldg(yq + 3);
+    uint4 qa = __ldg(yq), qb = __ldg(yq + 1);   // this sub's 8 column words; the next 8 load during it
     cd[0] = qa.x;
     uint32_t nsub = 0;
 
     for (uint32_t ch = 0; ch < nch; ++ch) {
 #pragma unroll kSU
       for (int sub = 0; sub < kChunk / 8; ++sub, ++nsub) {
-        const uint4 na = __ldg(yq + 2 * nsub + 4), nb = __ldg(yq + 2 * nsub + 5);
+        const uint4 na = __ldg(yq + 2 * nsub + 2), nb = __ldg(yq + 2 * nsub + 3);
         uint32_t* rs0 = ring0 + sub * 8;
         uint32_t* rs1 = ring1 + sub * 8;
 #pragma unroll
@@ -219,10 +194,10 @@ combd_kernel(const CombParams p) {
           uint2 nfx[K];
 #pragma unroll
           for (int b = 0; b < K; ++b) {
-            const uint32_t tbase = madhi(cd[b], tblmul, tlb);
+            const uint32_t tbase = imad(cd[b], one, tlb);   // column word = the code's table offset
 #pragma unroll
             for (int qq = 0; qq < QB; ++qq) nfq[b * QB + qq] = lds128(tbase + (b * QB + qq) * 16);
-            nfx[b] = lds64(madhi(cd[b], extmul, txb) + b * 256);
+            nfx[b] = lds64(tbase + (b + 1) * QB * 16);        // first two words of the quad below the band
           }
           uint32_t tin0[K], tin1[K];
           {
@@ -276,14 +251,14 @@ combd_kernel(const CombParams p) {
           }
           {
             const uint32_t ynew = u == 0 ? qa.y : u == 1 ? qa.z : u == 2 ? qa.w : u == 3 ? qb.x :
-                                  u == 4 ? qb.y : u == 5 ? qb.z : u == 6 ? qb.w : qc.x;
+                                  u == 4 ? qb.y : u == 5 ? qb.z : u == 6 ? qb.w : na.x;
             const uint32_t sh = shfl_up1<L>(cd[K - 1]);
 #pragma unroll
             for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
             cd[0] = imad(sh, nz, ynew);
           }
         }
-        qa = qc; qb = qd; qc = na; qd = nb;
+        qa = na; qb = nb;
       }
       __syncwarp();
 
