@@ -101,6 +101,7 @@ struct Shape {
 constexpr ShapeDef kDualShapes[] = {
     {4, 32, 1}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {8, 8, 2}, {4, 16, 2},
     {4, 32, 2}, {8, 32, 1}, {8, 16, 1}, {16, 16, 2}, {8, 8, 1},
+    {4, 8, 2}, {4, 24, 2}, {8, 24, 2}, {16, 24, 2}, {32, 24, 2}, {16, 32, 2}, {32, 32, 2},
 };
 
 bool dual_shape_fits(uint32_t W, uint32_t sigma, bool dense, int l, int r, int k, int hf, Shape* out) {

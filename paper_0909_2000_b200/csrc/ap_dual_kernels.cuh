@@ -74,7 +74,7 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 #endif
 
 template <int L, int R, int K, bool DENSE, bool HF>
-__global__ void __launch_bounds__(32, R <= 8 ? 16 : (R <= 16 ? AP_DUAL_MINB16 : (L >= 8 ? AP_DUAL_MINB32_L8 : AP_DUAL_MINB32)))
+__global__ void __launch_bounds__(32, R <= 8 ? 16 : (R <= 24 ? AP_DUAL_MINB16 : (L == 32 ? 8 : (L >= 8 ? AP_DUAL_MINB32_L8 : AP_DUAL_MINB32))))
 combd_kernel(const CombParams p) {
   constexpr int kHfRows = HF ? AP_DUAL_HF_ROWS : 0;
   constexpr int kSU = AP_DUAL_SUBUNROLL;
