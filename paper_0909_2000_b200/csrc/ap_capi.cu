@@ -184,6 +184,7 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out, bool dual_
 // r = 2 specialised shapes (L, RR real rows per lane, K bands): usable when
 // RR divides w and w/RR <= L (idle trailing lanes are padding).
 struct Shape2Def { int L, RR, K; };
+
 constexpr Shape2Def kShapes2[] = {
     {4, 25, 5}, {8, 8, 2}, {8, 8, 4}, {16, 4, 2}, {16, 8, 4}, {32, 8, 4},
     {8, 16, 4}, {16, 16, 4}, {32, 16, 4}, {32, 4, 2},
@@ -191,9 +192,34 @@ constexpr Shape2Def kShapes2[] = {
     {10, 10, 2}, {5, 20, 4}, {10, 10, 1}, {5, 20, 1},
 };
 
-bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out) {
+// r = 2 dual-pair shape (comb2d_kernel): 4 real rows per lane, w = 4*L exactly
+bool dual2_shape_fits(uint32_t w, uint32_t sigma_y, bool dense, int l, int k, Shape* out) {
+  if (l <= 0 || w != uint32_t(4 * l) || !apk::pick_r2_dual(l, k, dense)) return false;
+  const uint32_t ring = apk::ring_slots(2 * w, 2 * apk::kChunk, l);
+  const size_t smem = apk::comb2d_smem_per_warp(l, sigma_y, ring);
+  if (smem > kSmemPerSm / 8) return false;   // keep at least 8 warps per SM
+  out->L = l; out->R = 8; out->K = k; out->xm = false; out->r2 = true; out->hf = false; out->dual = true;
+  out->ring = ring;
+  out->smem = smem * apk::kWarpsPerCta;   // rescaled to the launch's one-warp CTAs by the plan
+  out->warps_per_sm = 0;
+  return true;
+}
+
+bool choose_shape2(uint32_t w, uint32_t sigma_y, bool dense, Shape* out, bool dual_ok = false) {
   if (std::getenv("AP_NO_R2")) return false;
   const uint32_t W = 2 * w;
+  out->dual = false;
+  if (dual_ok) {
+    if (const char* env = std::getenv("AP_SHAPE2")) {   // "L,4,K,0,1": forced dual shape
+      int l = 0, rr = 0, k = 0, hf = 0, dual = 0;
+      if (std::sscanf(env, "%d,%d,%d,%d,%d", &l, &rr, &k, &hf, &dual) == 5 && dual && rr == 4 &&
+          dual2_shape_fits(w, sigma_y, dense, l, k, out))
+        return true;
+    }
+    // not chosen automatically: on C4 it runs at 53.8-54.8 ms per 16384 rows against 53.4 for
+    // comb2<16,4,2> (same instruction count: what the shared code feed saves, the second pair's
+    // selects, moves and ring stores cost; profiles/ab_r02.md)
+  }
   // fp16 keys need W + 2*VB <= kHfMaxSpan (VB = virtual bands down the strip)
   auto hf_ok = [&](int rr, int k) { return W + 2 * (w / uint32_t(rr)) * uint32_t(k) <= apk::kHfMaxSpan; };
   // tuning override: AP_SHAPE2="L,RR,K[,hf]" (hf: 0/1, default: the automatic choice)
@@ -783,7 +809,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   // 0.049 -> 0.058 ms); AP_DUAL=1 forces it for eligible plots
   const size_t max_nseg = std::max<size_t>(1, (N - W + 1) / std::max<size_t>(4 * W, 256));
   const char* dual_env = std::getenv("AP_DUAL");
-  const bool dual_ok = r == 1 && h == 1 &&
+  const bool dual_ok = h == 1 &&
                        (dual_env ? std::atoi(dual_env) != 0 : ((nrows + 1) / 2) * max_nseg >= size_t(16) * 12 * c->sms);
   const uint64_t pkey = (uint64_t(w) << 20) | (uint64_t(r) << 18) | (uint64_t(sigma_y) << 2) | (dual_ok ? 2 : 0) |
                         (dense ? 1 : 0);
@@ -792,11 +818,12 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   if (hit != c->plans.end()) {
     plan = hit->second;
   } else {
-    plan.spec = r == 2 && choose_shape2(w, sigma_y, dense, &plan.sh);
-    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh, dual_ok))
+    plan.spec = r == 2 && choose_shape2(w, sigma_y, dense, &plan.sh, dual_ok);
+    if (!plan.spec && !choose_shape(W, sigma, dense, &plan.sh, dual_ok && r == 1))
       return fail(AP_CONFIG, "alphabet of %u codes with blown window %u does not fit the engine's tables",
                   sigma, W);
-    plan.fn = plan.spec ? apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf)
+    plan.fn = plan.spec ? (plan.sh.dual ? apk::pick_r2_dual(plan.sh.L, plan.sh.K, dense)
+                                        : apk::pick_r2(plan.sh.L, plan.sh.R / 2, plan.sh.K, dense, plan.sh.hf))
               : plan.sh.dual ? apk::pick_dual(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.hf)
                         : pick_kernel(plan.sh.L, plan.sh.R, plan.sh.K, dense, plan.sh.xm, plan.sh.hf);
     if (!plan.fn) return fail(AP_CONFIG, "no kernel instantiation for L=%d R=%d", plan.sh.L, plan.sh.R);
@@ -812,8 +839,8 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const Shape& sh = plan.sh;
   const bool spec = plan.spec;
   if (spec)
-    std::snprintf(c->last_kernel, sizeof(c->last_kernel), "comb2<%d,%d,%d,%s>", sh.L, sh.R / 2, sh.K,
-                  sh.hf ? "fp16" : "int");
+    std::snprintf(c->last_kernel, sizeof(c->last_kernel), "%s<%d,%d,%d,%s>", sh.dual ? "comb2d" : "comb2", sh.L,
+                  sh.R / 2, sh.K, sh.hf ? "fp16" : "int");
   else
     std::snprintf(c->last_kernel, sizeof(c->last_kernel), "%s<%d,%d,%d,%s,%s>", sh.dual ? "combd" : "comb", sh.L,
                   sh.R, sh.K, sh.xm ? "computed" : "table", sh.hf ? "fp16" : "int");
@@ -828,12 +855,15 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t ylen = spec ? n : N;
   const size_t ytot = (ylen + 256 + 31) / 32 * 32;
   if ((rc = grow(&c->d_ycode, &c->cap_ycode, ytot))) return rc;
-  if (!spec && (rc = grow(&c->d_ycol, &c->cap_ycol, 2 * ytot))) return rc;   // ytot: multiple of 32
+  const bool want_ycol = !spec || sh.dual;   // column-word stream (generic kernels and both dual kernels)
+  if (want_ycol && (rc = grow(&c->d_ycol, &c->cap_ycol, 2 * ytot))) return rc;   // ytot: multiple of 32
   // column words: the code in both halves, or for the dual-pair kernel its table offset
-  const uint32_t ycol_mult = sh.dual ? uint32_t(sh.L * apk::dual_pj(sh.L, sh.R) * 16) : 0x00010001u;
+  const uint32_t ycol_mult = !sh.dual ? 0x00010001u
+                             : spec   ? uint32_t(apk::r2d_nq(sh.L) * 16)
+                                      : uint32_t(sh.L * apk::dual_pj(sh.L, sh.R) * 16);
   if (fused_codes) {
     apk::codes_small_kernel<<<1, 1024, 0, st>>>(d_x, mx, d_y, n, spec ? 1 : r, sent, c->d_map, c->d_small,
-                                                c->d_xcode, c->d_ycode, ytot, spec ? nullptr : c->d_ycol, ycol_mult);
+                                                c->d_xcode, c->d_ycode, ytot, want_ycol ? c->d_ycol : nullptr, ycol_mult);
     CK(cudaGetLastError());
     c->last_launches += 1;
   } else {
@@ -841,7 +871,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
                                                                                  c->d_xcode);
     CK(cudaGetLastError());
     apk::ycode_kernel<<<std::min<size_t>((ytot + 255) / 256, 4096), 256, 0, st>>>(
-        d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot, spec ? nullptr : c->d_ycol, ycol_mult);
+        d_y, n, spec ? 1 : r, sent, c->d_map, c->d_ycode, ytot, want_ycol ? c->d_ycol : nullptr, ycol_mult);
     CK(cudaGetLastError());
     c->last_launches += 3;
   }
@@ -877,7 +907,7 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   p.xcode = c->d_xcode;
   p.ycode = c->d_ycode;
   p.ycol = c->d_ycol;
-  p.ycol_zero = spec ? nullptr : c->d_ycol + ytot;
+  p.ycol_zero = want_ycol ? c->d_ycol + ytot : nullptr;
   p.rows = uint32_t(nrows);
   p.xlen = uint32_t(mx);
   p.h = h;

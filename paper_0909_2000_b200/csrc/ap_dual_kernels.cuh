@@ -331,4 +331,296 @@ combd_kernel(const CombParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dual-pair alignment-score kernel (r = 2, h = 1, w = 4*L): comb2_kernel's cell classes
+// (ap_kernels.cuh: ($,$) swap free, ($,real) / (real,$) compare-exchange, real x real table
+// cell) with two strip pairs per lane group.  A lane holds RR = 4 real rows (8 blown rows) of
+// both pairs; pair 1's mask word of real row i is pair 0's of row i + 2, so a step reads 6
+// words.  One linear table per warp, T[code][warp real row / 4]: group g's rows are group 0's
+// shifted by 4 = one quad, lane (g, j) reads quad g + j, so every quarter warp of an LDS.128
+// reads 8 consecutive quads (conflict-free) and the table is 16 * (G + L) bytes per code, rounded
+// up to 128, instead of 512 (C4, 20 codes: 7.7 KB per warp).  The per-step overhead of comb2_kernel (code
+// feed, table address, shuffles, ring stores: 16 of 44 issue slots on C4) is shared by twice
+// the cells.
+KernelFn pick_r2_dual(int l, int k, bool dense);
+
+// table quads per code: G + L, rounded up to 8 quads (128 B) so that lanes holding different
+// codes (lane j is at column s - j) still fall on bank group (g + j) mod 8
+__host__ __device__ constexpr int r2d_nq(int L) { return (32 / L + L + 7) / 8 * 8; }
+__host__ __device__ inline size_t comb2d_smem_per_warp(int L, uint32_t sigma, uint32_t ring) {
+  const int G = 32 / L;
+  const size_t bytes = size_t(16) * sigma * r2d_nq(L)
+       + ((size_t(2) * G * ring_stride(L, 2 * kChunk) * 4 + 15) & ~size_t(15))
+       + size_t(G) * ok_stride(ring);
+  return (bytes + 15) & ~size_t(15);
+}
+
+#ifndef AP_R2D_MINB
+#define AP_R2D_MINB 16
+#endif
+#ifndef AP_R2D_SUBUNROLL
+#define AP_R2D_SUBUNROLL 2
+#endif
+
+template <int L, int K, bool DENSE>
+__global__ void __launch_bounds__(32, AP_R2D_MINB)
+comb2d_kernel(const CombParams p) {
+  static_assert(32 % L == 0 && L >= 4 && (K == 1 || K == 2), "bad shape");
+  constexpr int G = 32 / L;
+  constexpr int RR = 4;            // real rows per lane
+  constexpr int R = 2 * RR;        // blown rows per lane
+  constexpr int RRB = RR / K;      // real rows per band
+  constexpr int NB = 2 * kChunk;   // blown bottom columns per chunk
+  constexpr int kSU2 = AP_R2D_SUBUNROLL;
+  constexpr int NQ = r2d_nq(L);    // table quads per code (G + L used)
+  constexpr int VB = L * K;
+  extern __shared__ __align__(16) unsigned char smem[];
+
+  const uint32_t lane = lane_id();
+  const uint32_t g = lane / L;
+  const uint32_t j = lane % L;
+  uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][NQ]
+  const size_t tbytes = size_t(p.sigma) * NQ * 16;
+  constexpr int RS = ring_stride(L, NB);
+  uint32_t* ring0 = reinterpret_cast<uint32_t*>(smem + tbytes) + g * RS;
+  uint32_t* ring1 = ring0 + G * RS;
+  const uint32_t okb = uint32_t(__cvta_generic_to_shared(smem + tbytes)) +
+                       ((2 * G * RS * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
+
+  const uint32_t npairs = (p.rows + 1) / 2;
+  const uint32_t ngroups = (npairs + 2 * G - 1) / (2 * G);
+  const uint32_t gsplit = min(p.g_split, ngroups);
+  const uint64_t split_tasks = uint64_t(gsplit) * p.nseg;
+  const uint64_t ntasks = split_tasks + uint64_t(ngroups - gsplit) * p.nseg2;
+  const uint64_t wstride = uint64_t(gridDim.x);
+  if (p.sigma_cap != 0xFFFFFFFFu && *p.sigma_dev > p.sigma_cap) {   // speculative plan too small
+    if (threadIdx.x == 0) *p.abort_flag = 1u;
+    return;
+  }
+
+  for (uint64_t task = blockIdx.x; task < ntasks; task = next_task(p, task, wstride, lane, ntasks)) {
+    CombParams pt = p;
+    uint32_t pg, seg;
+    if (task < split_tasks) {
+      pg = uint32_t(task / p.nseg);
+      seg = uint32_t(task % p.nseg);
+    } else {
+      pg = gsplit + uint32_t((task - split_tasks) / p.nseg2);
+      seg = uint32_t((task - split_tasks) % p.nseg2);
+      pt.S = p.S2;
+    }
+    const uint32_t r0 = 4 * (pg * G + g);
+    const bool has0 = r0 < p.rows, has1 = r0 + 1 < p.rows, has2 = r0 + 2 < p.rows, has3 = r0 + 3 < p.rows;
+    const uint32_t c0 = seg * pt.S;                        // blown, multiple of 64
+    const uint32_t c0r = c0 >> 1;                          // raw, multiple of 32
+    const uint32_t nseg_cols = min(pt.S + p.W - 1, p.N - c0);
+    const uint32_t nraw = (nseg_cols + 1) >> 1;
+    const uint32_t nsteps = nraw + VB - 1;
+    const uint32_t nch = (nsteps + kChunk - 1) / kChunk;
+
+    // ---- mask table (real rows, real codes): word of warp real row u = (x[rw+u] == a) |
+    // (x[rw+1+u] == a) << 16, rw = the first grid row of the warp's group 0
+    __syncwarp();
+    {
+      const uint32_t rw = 4 * pg * G;
+      for (uint32_t c = lane; c < uint32_t(G + L); c += 32) {
+        uint32_t xc[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const uint32_t idx = rw + 4 * c + k;
+          uint32_t cv = 0x1FFu;
+          if (idx < p.xlen) {
+            cv = p.xcode[idx];
+            if (cv == 0xFFu) cv = 0x1FFu;
+          }
+          xc[k] = cv;
+        }
+        for (uint32_t a = 0; a < p.sigma; ++a) {
+          uint32_t wv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            wv[k] = (xc[k] == a ? 0x00008000u : 0u) | (xc[k + 1] == a ? 0x80000000u : 0u);
+          tbl[a * NQ + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      }
+      for (uint32_t k = j; k < p.ring; k += L) sts_u32(okb + 4 * k, 0u);
+    }
+    __syncwarp();
+
+    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + g + j));
+    const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0r);
+    const uint32_t nz = j != 0 ? 1u : 0u;
+    const uint32_t finc = j == 0 ? 0x00020002u : 0u;
+    const uint32_t one = p.one;
+
+    uint32_t V0[R], V1[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) { V0[i] = 0u; V1[i] = 0u; }
+    uint32_t tbD0[K], tbR0[K], tbD1[K], tbR1[K], cd[K];
+#pragma unroll
+    for (int b = 0; b < K; ++b) { tbD0[b] = 0u; tbR0[b] = 0u; tbD1[b] = 0u; tbR1[b] = 0u; cd[b] = 0u; }
+    int32_t kbase = -int32_t(p.W) - 1;
+    uint32_t freshD = j == 0 ? uint32_t(-kbase) * 0x00010001u : 0u;   // key of blown column 2s (lane 0)
+    uint32_t freshR = j == 0 ? freshD + 0x00010001u : 0u;             // ... and of 2s + 1
+    uint32_t run0 = 0u, run1 = 0u, hits0 = 0u, hits1 = 0u, hits2 = 0u, hits3 = 0u;
+
+    uint4 qa = __ldg(yq), qb = __ldg(yq + 1);
+    cd[0] = qa.x;
+    uint32_t nsub = 0;
+
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+#pragma unroll kSU2
+      for (int sub = 0; sub < kChunk / 8; ++sub, ++nsub) {
+        const uint4 na = __ldg(yq + 2 * nsub + 2), nb = __ldg(yq + 2 * nsub + 3);
+        uint32_t* rs0 = ring0 + sub * 16;
+        uint32_t* rs1 = ring1 + sub * 16;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          // mask words of this step: band b needs real rows [b*RRB, b*RRB + RRB + 2)
+          uint32_t m[K][RRB + 2];
+          if constexpr (K == 1) {
+            const uint32_t tbase = imad(cd[0], one, tlb);
+            const uint4 w4 = lds128(tbase);
+            const uint2 w2 = lds64(tbase + 16);
+            m[0][0] = w4.x; m[0][1] = w4.y; m[0][2] = w4.z; m[0][3] = w4.w; m[0][4] = w2.x; m[0][5] = w2.y;
+          } else {
+            const uint4 w4 = lds128(imad(cd[0], one, tlb));
+            m[0][0] = w4.x; m[0][1] = w4.y; m[0][2] = w4.z; m[0][3] = w4.w;
+            const uint32_t tb1 = imad(cd[K - 1], one, tlb);
+            const uint2 wa = lds64(tb1 + 8), wb = lds64(tb1 + 16);
+            m[K - 1][0] = wa.x; m[K - 1][1] = wa.y; m[K - 1][2] = wb.x; m[K - 1][3] = wb.y;
+          }
+          uint32_t tinD0[K], tinR0[K], tinD1[K], tinR1[K];
+          {
+            const uint32_t a0 = shfl_up1<L>(tbD0[K - 1]);
+            const uint32_t a1 = shfl_up1<L>(tbR0[K - 1]);
+            const uint32_t a2 = shfl_up1<L>(tbD1[K - 1]);
+            const uint32_t a3 = shfl_up1<L>(tbR1[K - 1]);
+            tinD0[0] = imad(a0, nz, freshD);
+            tinR0[0] = imad(a1, nz, freshR);
+            tinD1[0] = imad(a2, nz, freshD);
+            tinR1[0] = imad(a3, nz, freshR);
+#pragma unroll
+            for (int b = 1; b < K; ++b) {
+              tinD0[b] = tbD0[b - 1]; tinR0[b] = tbR0[b - 1];
+              tinD1[b] = tbD1[b - 1]; tinR1[b] = tbR1[b - 1];
+            }
+          }
+          freshD = imad(freshD, one, finc);
+          freshR = imad(freshR, one, finc);
+#pragma unroll
+          for (int b = 0; b < K; ++b) {
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              uint32_t* V = pr ? V1 : V0;
+              uint32_t t = pr ? tinD1[b] : tinD0[b];           // blown column 2c: $
+#pragma unroll
+              for (int i = 0; i < RRB; ++i) {
+                uint32_t& vs = V[b * 2 * RRB + 2 * i];         // $ row: match -> swap
+                const uint32_t sw = vs;
+                vs = t;
+                t = sw;
+                uint32_t& vr = V[b * 2 * RRB + 2 * i + 1];     // real row: mismatch
+                const uint32_t d = __vmaxu2(vr, t);
+                vr = __vminu2(vr, t);
+                t = d;
+              }
+              (pr ? tbD1[b] : tbD0[b]) = t;
+              t = pr ? tinR1[b] : tinR0[b];                    // blown column 2c+1: real character
+#pragma unroll
+              for (int i = 0; i < RRB; ++i) {
+                uint32_t& vs = V[b * 2 * RRB + 2 * i];         // $ row: mismatch; min on the FMA pipe
+                const uint32_t d0 = __vmaxu2(vs, t);
+                vs = imad(d0, p.minus_one, imad(vs, one, t));  // vs + t - max (16-bit halves never carry)
+                t = d0;
+                uint32_t& vr = V[b * 2 * RRB + 2 * i + 1];     // real x real: table
+                const uint32_t d1 = __viaddmax_s16x2(t, m[b][i + 2 * pr], vr);
+                vr = lop3_xor(vr, t, d1);
+                t = d1;
+              }
+              (pr ? tbR1[b] : tbR0[b]) = t;
+            }
+          }
+          if (j == L - 1) {
+            *reinterpret_cast<uint2*>(rs0 + 2 * u) = make_uint2(tbD0[K - 1], tbR0[K - 1]);
+            *reinterpret_cast<uint2*>(rs1 + 2 * u) = make_uint2(tbD1[K - 1], tbR1[K - 1]);
+          }
+          {
+            const uint32_t ynew = u == 0 ? qa.y : u == 1 ? qa.z : u == 2 ? qa.w : u == 3 ? qb.x :
+                                  u == 4 ? qb.y : u == 5 ? qb.z : u == 6 ? qb.w : na.x;
+            const uint32_t sh = shfl_up1<L>(cd[K - 1]);
+#pragma unroll
+            for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
+            cd[0] = imad(sh, nz, ynew);
+          }
+        }
+        qa = na; qb = nb;
+      }
+      __syncwarp();
+
+      // ---- window extraction of both pairs (shared ok-flag ring: bytes 0/2 and 1/3)
+      {
+        constexpr int CPL = NB / L;
+        const int32_t E0 = 2 * (int32_t(ch * kChunk) - int32_t(VB - 1));
+        const uint32_t rmask = p.ring - 1;
+        const bool interior = E0 >= int32_t(p.W) - 1 &&
+                              E0 + NB <= min(int32_t(nseg_cols), int32_t(pt.S + p.W) - 1);
+        uint32_t cab0[CPL], cab1[CPL], o[CPL], o0[CPL], o1[CPL];
+        if (interior) {
+          extract_scatter<L, NB, false, 0>(pt, ring0, okb, rmask, j, E0, nseg_cols, kbase, cab0);
+          extract_scatter<L, NB, false, 1>(pt, ring1, okb, rmask, j, E0, nseg_cols, kbase, cab1);
+          __syncwarp();
+          extract_flags<L, NB, false>(pt, okb, rmask, j, E0, nseg_cols, o);
+        } else {
+          extract_scatter<L, NB, true, 0>(pt, ring0, okb, rmask, j, E0, nseg_cols, kbase, cab0);
+          extract_scatter<L, NB, true, 1>(pt, ring1, okb, rmask, j, E0, nseg_cols, kbase, cab1);
+          __syncwarp();
+          extract_flags<L, NB, true>(pt, okb, rmask, j, E0, nseg_cols, o);
+        }
+        extract_clear<L, NB>(pt, okb, rmask, j, E0);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          o0[c] = o[c] & 0x00010001u;
+          o1[c] = (o[c] >> 8) & 0x00010001u;
+        }
+        if (interior) {
+          extract_out<L, NB, DENSE, false>(pt, j, g, lane, E0, nseg_cols, c0, cab0, o0, r0, r0 + 1, has0, has1,
+                                           run0, hits0, hits1);
+          extract_out<L, NB, DENSE, false>(pt, j, g, lane, E0, nseg_cols, c0, cab1, o1, r0 + 2, r0 + 3, has2, has3,
+                                           run1, hits2, hits3);
+        } else {
+          extract_out<L, NB, DENSE, true>(pt, j, g, lane, E0, nseg_cols, c0, cab0, o0, r0, r0 + 1, has0, has1,
+                                          run0, hits0, hits1);
+          extract_out<L, NB, DENSE, true>(pt, j, g, lane, E0, nseg_cols, c0, cab1, o1, r0 + 2, r0 + 3, has2, has3,
+                                          run1, hits2, hits3);
+        }
+      }
+
+      if (uint32_t(int32_t((ch + 2) * NB) - kbase) >= kRebaseAt) {
+        const uint32_t by = kRebaseBy * 0x00010001u;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          V0[i] = __vmaxu2(V0[i], by) - by;
+          V1[i] = __vmaxu2(V1[i], by) - by;
+        }
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          tbD0[b] = __vmaxu2(tbD0[b], by) - by; tbR0[b] = __vmaxu2(tbR0[b], by) - by;
+          tbD1[b] = __vmaxu2(tbD1[b], by) - by; tbR1[b] = __vmaxu2(tbR1[b], by) - by;
+        }
+        if (j == 0) { freshD -= by; freshR -= by; }
+        kbase += int32_t(kRebaseBy);
+      }
+    }
+    if constexpr (!DENSE) {
+      if (j == 0) {
+        if (has0) p.seg_counts[size_t(r0) * p.seg_stride + seg] = hits0;
+        if (has1) p.seg_counts[size_t(r0 + 1) * p.seg_stride + seg] = hits1;
+        if (has2) p.seg_counts[size_t(r0 + 2) * p.seg_stride + seg] = hits2;
+        if (has3) p.seg_counts[size_t(r0 + 3) * p.seg_stride + seg] = hits3;
+      }
+    }
+  }
+}
+
 }  // namespace apk

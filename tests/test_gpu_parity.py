@@ -321,6 +321,64 @@ def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
         assert np.array_equal(grid[rb:rb + 2], wr), rb
 
 
+@pytest.mark.parametrize("shape", ["8,4,1", "8,4,2", "16,4,1", "16,4,2", "32,4,1", "32,4,2"])
+def test_forced_r2_dual_shapes(shape, monkeypatch):
+    """The r = 2 dual-pair kernel (comb2d_kernel: two strip pairs per lane group, one linear mask
+    table per warp), w = 4 L, every row-count residue mod 4, dense and thresholded, a 20-letter
+    and a 4-letter alphabet."""
+    monkeypatch.setenv("AP_SHAPE2", shape + ",0,1")
+    monkeypatch.setenv("AP_DUAL", "1")
+    L, RR, K = map(int, shape.split(","))
+    w = 4 * L
+    rng = np.random.default_rng(L * 10 + K)
+    for extra in range(4):
+        sigma = 20 if extra % 2 else 4
+        x = rng.integers(1, sigma + 1, w + 90 + extra).astype(np.uint8)
+        y = np.concatenate([rng.integers(1, sigma + 1, 200), x[5:w + 60], rng.integers(1, sigma + 1, 300)]).astype(np.uint8)
+        if extra == 0:
+            name, grid = last_kernel_name(x, y, w, 1, 2)
+            assert name.startswith("comb2d<%d,4,%d," % (L, K)), name
+        rc, want = ol.plot_rows(x, y, w, 1, 2)
+        assert rc == 0
+        assert np.array_equal(gpu_grid(x, y, w, 1, 2), want), (shape, extra)
+        t = int(np.quantile(want, 0.97))
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (shape, extra)
+
+
+@pytest.mark.parametrize("w,sigma", [(64, 20), (32, 4), (128, 4)])
+def test_r2_dual_kernel_long_y_and_row_ranges(w, sigma, monkeypatch):
+    """comb2d_kernel (opt-in: AP_SHAPE2=L,4,K,0,1) on a y long enough for interior chunks and a
+    key rebase (> 28K blown columns) with planted homology, odd row ranges, a byte of x absent
+    from y, dense and thresholded."""
+    monkeypatch.setenv("AP_DUAL", "1")
+    monkeypatch.setenv("AP_SHAPE2", "%d,4,2,0,1" % (w // 4))
+    rng = np.random.default_rng(w + sigma + 1)
+    x = rng.integers(1, sigma + 1, w + 22).astype(np.uint8)
+    x[w // 2] = 200
+    parts = []
+    while sum(p.size for p in parts) < 20000:
+        parts.append(rng.integers(1, sigma + 1, int(rng.integers(50, 2500))).astype(np.uint8))
+        blk = x[int(rng.integers(0, 20)):][:w + 10].copy()
+        blk[blk == 200] = 1
+        flip = rng.random(blk.size) < 0.06
+        blk[flip] = rng.integers(1, sigma + 1, int(flip.sum()))
+        parts.append(blk)
+    y = np.concatenate(parts)
+    name, grid = last_kernel_name(x, y, w, 1, 2)
+    assert name.startswith("comb2d<"), name
+    rc, want = ol.plot_rows(x, y, w, 1, 2)
+    assert rc == 0 and np.array_equal(grid, want)
+    assert np.array_equal(gpu_grid(x, y, w, 1, 2), want)
+    for rb, re in ((1, 2), (3, 10), (5, 23), (22, 23)):
+        assert np.array_equal(gpu_grid(x, y, w, 1, 2, rb, re), want[rb:re]), (rb, re)
+    for t in (int(np.quantile(want, 0.999)), int(want.max())):
+        rr, cc = np.nonzero(want >= t)
+        gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 2), t)
+        assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), t
+
+
 R2_SHAPES = ["4,25,5", "4,25,1", "10,10,2", "10,10,1", "5,20,4", "5,20,1", "8,8,2", "8,8,4", "16,8,4",
              "32,8,4", "8,16,4", "16,16,4", "32,16,4", "16,4,2", "32,4,2", "16,10,2", "8,20,4", "32,5,1",
              "32,4,1", "16,4,1"]
