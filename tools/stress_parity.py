@@ -26,13 +26,23 @@ def main():
     a.add_argument("--seed", type=int, default=1)
     a.add_argument("--big", action="store_true", help="large windows (W up to 1024) and long y, few rows")
     a.add_argument("--wide", action="store_true", help="blown windows 1025..8000 (the large-window path), few rows")
+    a.add_argument("--dual", action="store_true",
+                   help="LCS plots with h = 1 and the dual-pair kernel's windows (AP_DUAL=1 lifts its size gate)")
     args = a.parse_args()
+    if args.dual:
+        os.environ["AP_DUAL"] = "1"
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
     cells = 0
     for it in range(args.n):
         r = 1 + int(rng.integers(0, 2))
-        if args.wide:
+        if args.dual:
+            r, h = 1, 1
+            w = int(rng.choice([32, 64, 64, 96, 128, 128, 192, 256, 256, 384, 512, 768, 1024]))
+            sigma = int(rng.choice([2, 4, 4, 20, 60]))
+            m = int(rng.integers(w, w + 300))
+            n = int(rng.integers(w, w + (40000 if it % 8 == 0 else 3000)))
+        elif args.wide:
             w = int(rng.integers(1025, 8001)) // r
             h = int(rng.choice([1, 1, 3]))
             sigma = int(rng.choice([2, 4, 4, 20]))
