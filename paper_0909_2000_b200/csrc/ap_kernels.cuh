@@ -234,6 +234,9 @@ constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: reba
 #ifndef AP_R2_PRMT
 #define AP_R2_PRMT 0   // r = 2 kernel: next code byte by one PRMT instead of SHF + LOP3
 #endif
+#ifndef AP_R2_IMADSEL
+#define AP_R2_IMADSEL 0   // r = 2 kernel: lane-0 key injection as IMAD(shuffled, nz, fresh) instead of SEL
+#endif
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -1071,6 +1074,11 @@ comb2_kernel(const CombParams p) {
     for (int b = 0; b < K; ++b) { tbD[b] = 0u; tbR[b] = 0u; cd[b] = 0u; }
     int32_t kbase = -int32_t(p.W) - 1 - (HF ? int32_t(kHfBase) : 0);
     uint32_t fresh = uint32_t(-kbase) * 0x00010001u;   // key of blown column 2s
+#if AP_R2_IMADSEL
+    const uint32_t nz2 = j != 0 ? 1u : 0u;
+    const uint32_t finc2 = j == 0 ? 0x00020002u : 0u;
+    uint32_t freshD0 = j == 0 ? fresh : 0u, freshR0 = j == 0 ? fresh + 0x00010001u : 0u;
+#endif
     // rebase step: with the fp16 encoding as large as keeps every seaweed that a
     // later window can count (starts >= the next chunk's E0 - W + 1)
     const uint32_t rebase_by = HF ? (kHfRebaseAt - kHfBase - 2 * kChunk - 2 * VB - p.W) & ~1u : kRebaseBy;
@@ -1123,12 +1131,22 @@ comb2_kernel(const CombParams p) {
           {
             const uint32_t shD = shfl_up1<L>(tbD[K - 1]);
             const uint32_t shR = shfl_up1<L>(tbR[K - 1]);
+#if AP_R2_IMADSEL
+            tinD[0] = imad(shD, nz2, freshD0);   // lane-0 injection on the FMA pipe (no SEL)
+            tinR[0] = imad(shR, nz2, freshR0);
+#else
             tinD[0] = j == 0 ? fresh : shD;
             tinR[0] = j == 0 ? fresh + 0x00010001u : shR;
+#endif
 #pragma unroll
             for (int b = 1; b < K; ++b) { tinD[b] = tbD[b - 1]; tinR[b] = tbR[b - 1]; }
           }
+#if AP_R2_IMADSEL
+          freshD0 = imad(freshD0, p.one, finc2);
+          freshR0 = imad(freshR0, p.one, finc2);
+#else
           fresh += 0x00020002u;
+#endif
 #pragma unroll
           for (int b = 0; b < K; ++b) {
             uint32_t t = tinD[b];                       // blown column 2c: $
@@ -1208,6 +1226,9 @@ comb2_kernel(const CombParams p) {
           tbR[b] = __vmaxu2(tbR[b], fl) - by;
         }
         fresh -= by;
+#if AP_R2_IMADSEL
+        if (j == 0) { freshD0 -= by; freshR0 -= by; }
+#endif
         kbase += int32_t(rebase_by);
       }
     }
