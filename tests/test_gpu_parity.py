@@ -296,6 +296,26 @@ def test_dual_kernel_long_y_and_row_ranges(w, sigma, monkeypatch):
         assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), t
 
 
+def test_dual_kernel_output_kinds(monkeypatch):
+    """uint8 / int32 half-units and the fused PGM raster (with and without a threshold) through
+    the dual-pair kernel equal the uint16 plot and the host-side quantisation."""
+    from paper_0909_2000_b200 import writers as wr
+    monkeypatch.setenv("AP_DUAL", "1")
+    rng = np.random.default_rng(64)
+    x = rng.integers(1, 5, 700).astype(np.uint8)
+    y = np.concatenate([x[100:400], rng.integers(1, 5, 500)]).astype(np.uint8)
+    name, _ = last_kernel_name(x, y, 64, 1, 1)
+    assert name.startswith("combd<"), name
+    rc, want = ol.plot_rows(x, y, 64, 1, 1)
+    c = cfg(64, 1, 1)
+    assert np.array_equal(ap.plot_dense_u8(x, y, c).astype(np.int32), want)
+    assert np.array_equal(ap.plot_dense_i32(x, y, c), want)
+    assert np.array_equal(ap.plot_dense_i32(x, y, c, 5, 42), want[5:42])
+    g = ap.PlotGrid(want.shape[0], want.shape[1], 64, 1, values=want.reshape(-1))
+    for t in (None, 90):
+        assert wr.plot_pgm(x, y, cfg(64, 1, 1, t)) == wr.pgm_header(*want.shape) + wr.pgm_pixels(g, t).tobytes()
+
+
 def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
     """Small plots keep the single-pair kernel (too few pair groups to fill the GPU), large ones
     take the dual-pair kernel; the streamed host plot (row blocks whose mask words reach into
