@@ -69,6 +69,12 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 #ifndef AP_DUAL_MINB16
 #define AP_DUAL_MINB16 12  // same for the R = 16 shapes
 #endif
+#ifndef AP_DUAL_HF_PHASE0
+#define AP_DUAL_HF_PHASE0 0   // which row of every four takes the fp16 form, pair 0 / pair 1
+#endif
+#ifndef AP_DUAL_HF_PHASE1
+#define AP_DUAL_HF_PHASE1 0
+#endif
 #ifndef AP_DUAL_SUBUNROLL
 #define AP_DUAL_SUBUNROLL 1
 #endif
@@ -225,14 +231,14 @@ combd_kernel(const CombParams p) {
               {
                 uint32_t& v = V0[b * RB + i];
                 const uint32_t d = __viaddmax_s16x2(t0, m[i], v);
-                if ((i & 3) < kHfRows) v = hadd2u(hsub2u(v, d), t0);
+                if (((i + AP_DUAL_HF_PHASE0) & 3) < kHfRows) v = hadd2u(hsub2u(v, d), t0);
                 else v = lop3_xor(v, t0, d);
                 t0 = d;
               }
               {
                 uint32_t& v = V1[b * RB + i];
                 const uint32_t d = __viaddmax_s16x2(t1, m[i + 2], v);
-                if ((i & 3) < kHfRows) v = hadd2u(hsub2u(v, d), t1);
+                if (((i + AP_DUAL_HF_PHASE1) & 3) < kHfRows) v = hadd2u(hsub2u(v, d), t1);
                 else v = lop3_xor(v, t1, d);
                 t1 = d;
               }
