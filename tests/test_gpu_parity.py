@@ -316,6 +316,24 @@ def test_dual_kernel_output_kinds(monkeypatch):
         assert wr.plot_pgm(x, y, cfg(64, 1, 1, t)) == wr.pgm_header(*want.shape) + wr.pgm_pixels(g, t).tobytes()
 
 
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_dual_kernel_row_shards(ndev, monkeypatch):
+    """Row shards (one GPU standing in for ndev devices) through the dual-pair kernel: shard
+    boundaries cut groups of four rows anywhere, each shard uploads its own x halo."""
+    monkeypatch.setenv("AP_DUAL", "1")
+    monkeypatch.setenv("AP_SHARDS_PER_DEVICE", str(ndev))
+    rng = np.random.default_rng(70 + ndev)
+    x = rng.integers(1, 5, 64 + 201).astype(np.uint8)
+    y = np.concatenate([x[30:230], rng.integers(1, 5, 400)]).astype(np.uint8)
+    rc, want = ol.plot_rows(x, y, 64, 1, 1)
+    many = ap.plot_dense_u16(x, y, cfg(64, 1, 1, n_devices=ndev)).astype(np.int32)
+    assert np.array_equal(many, want)
+    t = int(np.quantile(want, 0.97))
+    rr, cc = np.nonzero(want >= t)
+    gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(64, 1, 1, n_devices=ndev), t)
+    assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
+
+
 def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
     """Small plots keep the single-pair kernel (too few pair groups to fill the GPU), large ones
     take the dual-pair kernel; the streamed host plot (row blocks whose mask words reach into
