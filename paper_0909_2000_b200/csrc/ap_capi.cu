@@ -111,7 +111,9 @@ bool dual_shape_fits(uint32_t W, uint32_t sigma, bool dense, int l, int r, int k
   if (!apk::pick_dual(l, r, k, dense, hf)) return false;
   const uint32_t ring = apk::ring_slots(W, apk::kChunk, l);
   const size_t smem = apk::combd_smem_per_warp(l, r, k, sigma, ring);
-  if (smem > kSmemPerSm / 4) return false;   // keep at least 4 warps per SM
+  // at least 8 resident warps per SM (a large alphabet's table would crowd them out: the
+  // single-pair kernel with computed masks takes those plots); a forced shape only has to fit
+  if (smem > (std::getenv("AP_SHAPE") ? kSmemPerSm / 2 : kSmemPerSm / 8 - 1024)) return false;
   out->L = l; out->R = r; out->K = k; out->xm = false; out->hf = hf; out->dual = true; out->r2 = false;
   out->ring = ring;
   out->smem = smem * apk::kWarpsPerCta;   // shapes are recorded for 4-warp CTAs (rescaled by the plan)

@@ -349,6 +349,13 @@ def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
     rc, want = ol.plot_rows(x, y, 64, 1, 1)
     assert rc == 0 and np.array_equal(grid, want)
     assert np.array_equal(gpu_grid(x, y, 64, 1, 1), want)
+    # a 60-letter alphabet's table would leave fewer than 8 warps per SM: single-pair kernel
+    x60 = rng.integers(1, 61, 500).astype(np.uint8)
+    y60 = np.concatenate([x60[100:300], rng.integers(1, 61, 300)]).astype(np.uint8)
+    name, grid = last_kernel_name(x60, y60, 64, 1, 1)
+    assert name.startswith("comb<"), name
+    rc, want = ol.plot_rows(x60, y60, 64, 1, 1)
+    assert rc == 0 and np.array_equal(grid, want)
     monkeypatch.delenv("AP_DUAL")
     big_x = rng.integers(1, 5, 70000).astype(np.uint8)
     big_y = rng.integers(1, 5, 9000).astype(np.uint8)
