@@ -104,16 +104,15 @@ constexpr ShapeDef kDualShapes[] = {
     {4, 8, 2}, {4, 24, 2}, {8, 24, 2}, {16, 24, 2}, {32, 24, 2}, {16, 32, 2}, {32, 32, 2},
 };
 
-bool dual_shape_fits(uint32_t W, uint32_t sigma, bool dense, int l, int r, int k, int hf, Shape* out) {
+bool dual_shape_fits(uint32_t W, uint32_t sigma, bool dense, int l, int r, int k, int hf, Shape* out,
+                     size_t smem_limit = kSmemPerSm / 2) {
   if (uint32_t(l * r) != W) return false;
   if (hf < 0) hf = ghf_ok(W, l, k);
   if (hf && !ghf_ok(W, l, k)) return false;
   if (!apk::pick_dual(l, r, k, dense, hf)) return false;
   const uint32_t ring = apk::ring_slots(W, apk::kChunk, l);
   const size_t smem = apk::combd_smem_per_warp(l, r, k, sigma, ring);
-  // at least 8 resident warps per SM (a large alphabet's table would crowd them out: the
-  // single-pair kernel with computed masks takes those plots); a forced shape only has to fit
-  if (smem > (std::getenv("AP_SHAPE") ? kSmemPerSm / 2 : kSmemPerSm / 8 - 1024)) return false;
+  if (smem > smem_limit) return false;
   out->L = l; out->R = r; out->K = k; out->xm = false; out->hf = hf; out->dual = true; out->r2 = false;
   out->ring = ring;
   out->smem = smem * apk::kWarpsPerCta;   // shapes are recorded for 4-warp CTAs (rescaled by the plan)
@@ -137,8 +136,17 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out, bool dual_
     }
   }
   if (dual_ok && !std::getenv("AP_NO_DUAL") && !std::getenv("AP_SHAPE")) {
+    // first the measured order among shapes whose table leaves >= 8 warps per SM; a larger
+    // alphabet's table crowds the warps out, and with 2-6 resident warps the K = 2 shapes (four
+    // chains per lane) win: sigma = 60, w = 128: combd<8,16,2> 17.1 ms at 2 warps/SM against
+    // combd<4,32,1> 22.8 and the single-pair computed-mask kernel 23.0 (tools/sigma_cmp.sh); past
+    // ~90 KB per warp the single-pair kernel wins (sigma = 120, w = 64: 10.5 against 13.4-16.4)
     for (const ShapeDef& d : kDualShapes)
-      if (dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out)) return true;
+      if (dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out, kSmemPerSm / 8 - 1024)) return true;
+    for (int pass = 0; pass < 2; ++pass)
+      for (const ShapeDef& d : kDualShapes)
+        if ((d.K == 2) == (pass == 0) && dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out, 90 * 1024))
+          return true;
   }
   out->dual = false;
   double best = 1e30;

@@ -349,9 +349,9 @@ def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
     rc, want = ol.plot_rows(x, y, 64, 1, 1)
     assert rc == 0 and np.array_equal(grid, want)
     assert np.array_equal(gpu_grid(x, y, 64, 1, 1), want)
-    # a 60-letter alphabet's table would leave fewer than 8 warps per SM: single-pair kernel
-    x60 = rng.integers(1, 61, 500).astype(np.uint8)
-    y60 = np.concatenate([x60[100:300], rng.integers(1, 61, 300)]).astype(np.uint8)
+    # a 120-letter alphabet's table (> 90 KB per warp) keeps the single-pair kernel
+    x60 = rng.integers(1, 121, 500).astype(np.uint8)
+    y60 = np.concatenate([x60[100:300], rng.integers(1, 121, 300)]).astype(np.uint8)
     name, grid = last_kernel_name(x60, y60, 64, 1, 1)
     assert name.startswith("comb<"), name
     rc, want = ol.plot_rows(x60, y60, 64, 1, 1)
