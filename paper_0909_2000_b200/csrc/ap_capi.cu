@@ -865,10 +865,12 @@ int run_device(ap_ctx* c, const uint8_t* d_x, size_t mx, const uint8_t* d_y, siz
   const size_t ylen = spec ? n : N;
   const size_t ytot = (ylen + 256 + 31) / 32 * 32;
   if ((rc = grow(&c->d_ycode, &c->cap_ycode, ytot))) return rc;
-  const bool want_ycol = !spec || sh.dual;   // column-word stream (generic kernels and both dual kernels)
+  // column-word stream: generic kernels, both dual kernels, and the unrolled r = 2 shapes' feed
+  const bool r2_ycol = spec && !sh.dual && apk::r2_ycol_feed(sh.R / 2, sh.K);
+  const bool want_ycol = !spec || sh.dual || r2_ycol;
   if (want_ycol && (rc = grow(&c->d_ycol, &c->cap_ycol, 2 * ytot))) return rc;   // ytot: multiple of 32
   // column words: the code in both halves, or for the dual-pair kernel its table offset
-  const uint32_t ycol_mult = !sh.dual ? 0x00010001u
+  const uint32_t ycol_mult = r2_ycol ? uint32_t(sh.R / 2 * 128) : !sh.dual ? 0x00010001u
                              : spec   ? uint32_t(apk::r2d_nq(sh.L) * 16)
                                       : uint32_t(sh.L * apk::dual_pj(sh.L, sh.R) * 16);
   if (fused_codes) {

@@ -237,6 +237,13 @@ constexpr uint32_t kHfMaxSpan = 0x3C0u - 2 * 32 - 128;   // W + 2*VB bound: reba
 #ifndef AP_R2_IMADSEL
 #define AP_R2_IMADSEL 0   // r = 2 kernel: lane-0 key injection as IMAD(shuffled, nz, fresh) instead of SEL
 #endif
+#ifndef AP_R2_YCOL
+#define AP_R2_YCOL 0   // r = 2 kernel, unrolled shapes: u32 column words (code * table stride) instead of code bytes
+#endif
+// shapes of the r = 2 kernel that take the column-word feed: fully unrolled sub loop and one table array
+__host__ __device__ constexpr bool r2_ycol_feed(int rr, int k) {
+  return AP_R2_YCOL && rr <= AP_SUBUNROLL2_RR && ((rr / k) % 4 == 0 || (rr / k) < 4);
+}
 #ifndef AP_R2_MB4
 #define AP_R2_MB4 10  // r = 2 kernels with RR <= this are compiled for 4 CTAs per SM (C2: 6.87 -> 6.59 ms)
 #endif
@@ -972,6 +979,7 @@ comb2_kernel(const CombParams p) {
   constexpr int kSubUnroll2 = RR <= AP_SUBUNROLL2_RR ? kChunk / 8 : 1;
   constexpr bool kFmaMin = RR >= AP_FMAMIN_RR;  // one of the two mismatch mins moves to the FMA pipe
   constexpr bool kSubLoad = AP_R2_SUBLOAD && kSubUnroll2 == 1;   // C2 -0.5%; unrolled shapes: +3.7% (C4)
+  constexpr bool kYcol = r2_ycol_feed(RR, K);
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
@@ -1089,7 +1097,18 @@ comb2_kernel(const CombParams p) {
     // step's code) per sub s, prefetched one sub ahead, instead of selecting by sub index
     uint32_t w0n = 0, w1n = 0, w2n = 0, wi = 3;
     uint4 ych = make_uint4(0, 0, 0, 0), ych2 = ych;
-    if constexpr (kSubLoad) {
+    // column-word feed (kYcol): 8 words per sub from a register queue, the next 8 in flight;
+    // a band's table address is IMAD(word, 1, lane base)
+    const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0r);
+    uint4 qa = make_uint4(0, 0, 0, 0), qb = qa;
+    uint32_t nsubq = 0;
+    const uint32_t nzy = j != 0 ? 1u : 0u;
+    const uint32_t tq32 = uint32_t(__cvta_generic_to_shared(tq0));
+    const uint32_t tr32 = uint32_t(__cvta_generic_to_shared(tr0));
+    if constexpr (kYcol) {
+      qa = __ldg(yq); qb = __ldg(yq + 1);
+      cd[0] = qa.x;
+    } else if constexpr (kSubLoad) {
       w0n = __ldg(yw); w1n = __ldg(yw + 1); w2n = __ldg(yw + 2);
       if (j == 0) cd[0] = w0n & 0xFFu;
     } else {
@@ -1106,8 +1125,13 @@ comb2_kernel(const CombParams p) {
       }
 #pragma unroll kSubUnroll2
       for (int sub = 0; sub < kChunk / 8; ++sub) {
-        uint32_t w0, w1, w2;
-        if constexpr (kSubLoad) {
+        uint32_t w0 = 0, w1 = 0, w2 = 0;
+        uint4 na = make_uint4(0, 0, 0, 0), nb = na;
+        if constexpr (kYcol) {
+          na = __ldg(yq + 2 * nsubq + 2);
+          nb = __ldg(yq + 2 * nsubq + 3);
+          ++nsubq;
+        } else if constexpr (kSubLoad) {
           w0 = w0n; w1 = w1n; w2 = w2n;
           w0n = w2n;
           w1n = __ldg(yw + wi);
@@ -1124,8 +1148,20 @@ comb2_kernel(const CombParams p) {
           uint32_t m[K][RRB];
 #pragma unroll
           for (int b = 0; b < K; ++b) {
-            const uint32_t ab = cd[b] * K + b;
-            load_band_words<RRB>(tq0 + ab * (Q4 * 32), tr0 + ab * (32 * REM), m[b]);
+            if constexpr (kYcol) {
+              if constexpr (Q4 == 0) {
+                const uint32_t a = imad(cd[b], p.one, tr32) + b * (32 * REM * 4);
+                if constexpr (REM == 2) lds_v2(a, m[b]);
+                else m[b][0] = lds_u32(a);
+              } else {
+                const uint32_t a = imad(cd[b], p.one, tq32) + b * (Q4 * 512);
+#pragma unroll
+                for (int q = 0; q < Q4; ++q) lds_v4(a + q * 512, m[b] + 4 * q);
+              }
+            } else {
+              const uint32_t ab = cd[b] * K + b;
+              load_band_words<RRB>(tq0 + ab * (Q4 * 32), tr0 + ab * (32 * REM), m[b]);
+            }
           }
           uint32_t tinD[K], tinR[K];
           {
@@ -1195,7 +1231,14 @@ comb2_kernel(const CombParams p) {
               ring_sub[2 * u + 1] = tbR[K - 1];
             }
           }
-          {
+          if constexpr (kYcol) {
+            const uint32_t ynew = u == 0 ? qa.y : u == 1 ? qa.z : u == 2 ? qa.w : u == 3 ? qb.x :
+                                  u == 4 ? qb.y : u == 5 ? qb.z : u == 6 ? qb.w : na.x;
+            const uint32_t sh = shfl_up1<L>(cd[K - 1]);
+#pragma unroll
+            for (int b = K - 1; b > 0; --b) cd[b] = cd[b - 1];
+            cd[0] = imad(sh, nzy, ynew);
+          } else {
             const uint32_t ww = u < 3 ? w0 : (u < 7 ? w1 : w2);
 #if AP_R2_PRMT
             const uint32_t ynew = __byte_perm(ww, 0u, 0x4440u | uint32_t((u + 1) & 3));   // one PRMT
@@ -1208,6 +1251,7 @@ comb2_kernel(const CombParams p) {
             cd[0] = j == 0 ? ynew : sh;
           }
         }
+        if constexpr (kYcol) { qa = na; qb = nb; }
       }
       ych = nxa;
       ych2 = nxb;
