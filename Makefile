@@ -7,7 +7,7 @@ PKG := paper_0909_2000_b200
 CSRC := $(PKG)/csrc
 BUILD ?= build
 LIB ?= $(PKG)/libalignplot_b200.so
-OBJS := $(BUILD)/ap_capi.o $(BUILD)/ap_inst_l4.o $(BUILD)/ap_inst_l8.o $(BUILD)/ap_inst_l16.o $(BUILD)/ap_inst_l32.o $(BUILD)/ap_inst_r2.o $(BUILD)/ap_inst_r2hf.o $(BUILD)/ap_inst_ghf_a.o $(BUILD)/ap_inst_ghf_b.o $(BUILD)/ap_inst_ghf_c.o $(BUILD)/ap_inst_dual_a.o $(BUILD)/ap_inst_dual_b.o $(BUILD)/ap_inst_dual_c.o $(BUILD)/ap_inst_dual_r2.o
+OBJS := $(BUILD)/ap_capi.o $(BUILD)/ap_inst_l4.o $(BUILD)/ap_inst_l8.o $(BUILD)/ap_inst_l16.o $(BUILD)/ap_inst_l32.o $(BUILD)/ap_inst_r2.o $(BUILD)/ap_inst_r2hf.o $(BUILD)/ap_inst_ghf_a.o $(BUILD)/ap_inst_ghf_b.o $(BUILD)/ap_inst_ghf_c.o $(BUILD)/ap_inst_dual_a.o $(BUILD)/ap_inst_dual_b.o $(BUILD)/ap_inst_dual_c.o $(BUILD)/ap_inst_dual_d.o $(BUILD)/ap_inst_dual_r2.o
 HDRS := $(CSRC)/ap_kernels.cuh $(CSRC)/ap_aux_kernels.cuh $(CSRC)/ap_wide_kernels.cuh $(CSRC)/ap_dual_kernels.cuh include/alignplot_b200.h
 
 all: $(LIB) oracle

@@ -32,22 +32,51 @@ namespace apk {
 
 KernelFn pick_dual(int l, int r, int k, bool dense, bool hf);
 
-// quads between the table runs of consecutive lane indices j (odd: conflict-free LDS.128)
-// An LDS.128 is served a quarter warp (8 lanes, 128 B) at a time: for L >= 8 those are 8 lane
-// indices j of one group (PJ odd: 8 different bank groups), for L = 4 four j of two adjacent
-// groups (PJ = 2 mod 4: chunks 2j' + {0, 1}).
-__host__ __device__ constexpr int dual_pj(int L, int R) {
-  const int need = 32 / L + R / 4;
-  return L >= 8 ? (need | 1) : need + (6 - need % 4) % 4;
-}
-
-// Shared memory per warp (one-warp CTAs): the mask table [sigma][L][PJ] quads, two bottom-key
-// rings per group, one ok-flag ring per group.
-__host__ __device__ inline size_t combd_smem_per_warp(int L, int R, int K, uint32_t sigma, uint32_t ring) {
+// Quads between the table runs of consecutive lane indices j.  An LDS.128 is served a quarter
+// warp (8 lanes, 128 B) at a time, so PJ is the smallest run length for which the chunks
+// PJ*j + g of every aligned group of 8 lanes fall on 8 different bank groups (PJ odd for L >= 8,
+// PJ = 2 mod 4 for L = 4, 13 for L = 5; lane groups of 10 or 20 lanes straddle the quarters and
+// keep a 2-way conflict in some of them).
+__host__ __device__ constexpr int dual_pj_conflicts(int L, int PJ) {
   const int G = 32 / L;
-  const size_t bytes = size_t(16) * sigma * L * dual_pj(L, R)
-       + ((size_t(2) * G * ring_stride(L, kChunk) * 4 + 15) & ~size_t(15))
-       + size_t(G) * ok_stride(ring);
+  int worst = 0;
+  for (int a = 0; a < 32; ++a) {
+    const int ga = a / L < G ? a / L : G - 1, ca = PJ * (a % L) + ga;
+    int n = 1;
+    for (int b = (a / 8) * 8; b < (a / 8) * 8 + 8; ++b) {
+      const int gb = b / L < G ? b / L : G - 1, cb = PJ * (b % L) + gb;
+      bool first = true;   // count each distinct conflicting chunk once
+      for (int c = (a / 8) * 8; c < b; ++c) {
+        const int gc = c / L < G ? c / L : G - 1;
+        if (PJ * (c % L) + gc == cb) first = false;
+      }
+      if (b != a && cb != ca && cb % 8 == ca % 8 && first) ++n;
+    }
+    if (n > worst) worst = n;
+  }
+  return worst;
+}
+__host__ __device__ constexpr int dual_pj(int L, int R) {
+  const int need = 32 / L + R / 4 + (32 % L ? 1 : 0);
+  int best = need, bc = 99;
+  for (int pj = need; pj < need + 9; ++pj) {
+    const int c = dual_pj_conflicts(L, pj);
+    if (c < bc) { bc = c; best = pj; }
+  }
+  return best;
+}
+// table quads per code: the L runs, rounded up to 8 quads (128 B) so that lanes holding different
+// codes (lane j is at column s - j*K - b) keep their bank group
+__host__ __device__ constexpr int dual_cs(int L, int R) { return (L * dual_pj(L, R) + 7) / 8 * 8; }
+
+// Shared memory per warp (one-warp CTAs): the mask table [sigma][CS] quads, two bottom-key rings
+// per group, one ok-flag ring per group; lane groups that do not tile the warp (L = 5, 10, 20)
+// add an idle "phantom" group with its own rings and a 64-byte flag scratch (as comb2_kernel).
+__host__ __device__ inline size_t combd_smem_per_warp(int L, int R, int K, uint32_t sigma, uint32_t ring) {
+  const int G = 32 / L, Ga = groups_alloc(L);
+  const size_t bytes = size_t(16) * sigma * dual_cs(L, R)
+       + ((size_t(2) * Ga * ring_stride(L, kChunk) * 4 + 15) & ~size_t(15))
+       + size_t(G) * ok_stride(ring) + (Ga > G ? 64 : 0);
   return (bytes + 15) & ~size_t(15);
 }
 
@@ -84,9 +113,11 @@ __global__ void __launch_bounds__(32, R <= 8 ? 16 : (R <= 24 ? AP_DUAL_MINB16 : 
 combd_kernel(const CombParams p) {
   constexpr int kHfRows = HF ? AP_DUAL_HF_ROWS : 0;
   constexpr int kSU = AP_DUAL_SUBUNROLL;
-  static_assert(32 % L == 0 && L >= 4, "lane groups must tile the warp");
+  static_assert(L >= 4 && L <= 32, "lane groups of 4..32 lanes");
   static_assert(R % (4 * K) == 0, "bands must hold whole LDS.128 quads");
-  constexpr int G = 32 / L;
+  constexpr int G = 32 / L;          // real groups; lanes >= G*L form an idle phantom group
+  constexpr int Ga = groups_alloc(L);
+  constexpr int CS = dual_cs(L, R);
   constexpr int Q = R / 4;
   constexpr int RB = R / K;
   constexpr int QB = RB / 4;
@@ -97,14 +128,16 @@ combd_kernel(const CombParams p) {
   const uint32_t lane = lane_id();
   const uint32_t g = lane / L;
   const uint32_t j = lane % L;
-  uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][L][PJ]
-  const size_t tbytes = size_t(p.sigma) * L * PJ * 16;
+  uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][CS]: L runs of PJ quads
+  const size_t tbytes = size_t(p.sigma) * CS * 16;
   constexpr size_t xbytes = 0;
   constexpr int RSG = ring_stride(L, kChunk);
   uint32_t* ring0 = reinterpret_cast<uint32_t*>(smem + tbytes + xbytes) + g * RSG;
-  uint32_t* ring1 = ring0 + G * RSG;
+  uint32_t* ring1 = ring0 + Ga * RSG;
   const uint32_t okb = uint32_t(__cvta_generic_to_shared(smem + tbytes + xbytes)) +
-                       ((2 * G * RSG * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
+                       ((2 * Ga * RSG * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
+  // the phantom group folds every ok slot onto its 64-byte scratch
+  const uint32_t okmask = g < uint32_t(G) ? p.ring - 1 : 0u;
 
   const uint32_t npairs = (p.rows + 1) / 2;
   const uint32_t ngroups = (npairs + 2 * G - 1) / (2 * G);
@@ -129,7 +162,9 @@ combd_kernel(const CombParams p) {
       pt.S = p.S2;
     }
     const uint32_t r0 = 4 * (pg * G + g);   // grid rows r0, r0+1 (pair 0) and r0+2, r0+3 (pair 1)
-    const bool has0 = r0 < p.rows, has1 = r0 + 1 < p.rows, has2 = r0 + 2 < p.rows, has3 = r0 + 3 < p.rows;
+    const bool real_g = g < uint32_t(G);
+    const bool has0 = real_g && r0 < p.rows, has1 = real_g && r0 + 1 < p.rows, has2 = real_g && r0 + 2 < p.rows,
+               has3 = real_g && r0 + 3 < p.rows;
     const uint32_t c0 = seg * pt.S;
     const uint32_t nseg_cols = min(pt.S + p.W - 1, p.N - c0);
     const uint32_t nsteps = nseg_cols + VB - 1;
@@ -158,14 +193,14 @@ combd_kernel(const CombParams p) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             wv[k] = (xc[k] == a ? 0x00008000u : 0u) | (xc[k + 1] == a ? 0x80000000u : 0u);
-          tbl[(a * L + jj) * PJ + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          tbl[a * CS + jj * PJ + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
-      for (uint32_t k = j; k < p.ring; k += L) sts_u32(okb + 4 * k, 0u);
+      for (uint32_t k = j; k <= okmask; k += L) sts_u32(okb + 4 * k, 0u);
     }
     __syncwarp();
 
-    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + j * PJ + g));
+    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + j * PJ + (real_g ? g : uint32_t(G - 1))));
     const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
     const uint32_t nz = j != 0 ? 1u : 0u;
     const uint32_t finc = j == 0 ? 0x00010001u : 0u;
@@ -270,9 +305,9 @@ combd_kernel(const CombParams p) {
 
       // ---- window extraction of both pairs (shared ok-flag ring: bytes 0/2 and 1/3)
       {
-        constexpr int CPL = kChunk / L;
+        constexpr int CPL = (kChunk + L - 1) / L;
         const int32_t E0 = int32_t(ch * kChunk) - (VB - 1);
-        const uint32_t rmask = p.ring - 1;
+        const uint32_t rmask = okmask;
         const bool interior = E0 >= int32_t(p.W) - 1 &&
                               E0 + kChunk <= min(int32_t(nseg_cols), int32_t(pt.S + p.W) - 1);
         uint32_t cab0[CPL], cab1[CPL], o[CPL], o0[CPL], o1[CPL];

@@ -11,8 +11,10 @@ static KernelFn pick(bool dense, bool hf) {
 
 KernelFn pick_dual_a(int l, int r, int k, bool dense, bool hf);
 KernelFn pick_dual_c(int l, int r, int k, bool dense, bool hf);
+KernelFn pick_dual_d(int l, int r, int k, bool dense, bool hf);
 KernelFn pick_dual(int l, int r, int k, bool dense, bool hf) {
   if (KernelFn f = pick_dual_c(l, r, k, dense, hf)) return f;
+  if (KernelFn f = pick_dual_d(l, r, k, dense, hf)) return f;
   if (r == 32) return pick_dual_a(l, r, k, dense, hf);
 #define AP_D(L, R, K) \
   if (l == L && r == R && k == K) return pick<L, R, K>(dense, hf);

@@ -209,7 +209,9 @@ def test_forced_generic_shapes(shape, monkeypatch):
 
 
 DUAL_SHAPES = ["4,32,1", "4,32,2", "8,32,1", "8,32,2", "8,16,1", "8,16,2", "16,16,1", "16,16,2", "8,8,1", "8,8,2",
-               "4,16,2", "4,8,2", "4,24,2", "8,24,2", "16,24,2", "32,24,2", "16,32,2", "32,32,2"]
+               "4,16,2", "4,8,2", "4,24,2", "8,24,2", "16,24,2", "32,24,2", "16,32,2", "32,32,2",
+               # lane groups that do not tile the warp (idle phantom group)
+               "5,20,1", "10,20,1", "5,16,2", "5,24,2", "5,32,2", "10,32,2"]
 
 
 def _dual_hf_ok(s):   # fp16 keys need W + L*K <= 768 (kHfMaxSpan)
@@ -265,7 +267,8 @@ def test_forced_dual_shapes(shape, monkeypatch):
         assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc]), (shape, extra)
 
 
-@pytest.mark.parametrize("w,sigma", [(64, 4), (128, 4), (256, 4), (128, 20), (256, 2)])
+@pytest.mark.parametrize("w,sigma", [(64, 4), (128, 4), (256, 4), (128, 20), (256, 2), (100, 4), (200, 4), (100, 20),
+                                     (320, 4)])
 def test_dual_kernel_long_y_and_row_ranges(w, sigma, monkeypatch):
     """The dual-pair kernel as the default plan picks it (AP_DUAL=1 lifts the problem-size gate):
     a y long enough for interior chunks and fp16-key rebases with planted homology, odd row
