@@ -99,8 +99,8 @@ struct Shape {
 // Dual-pair shapes (combd_kernel, ap_dual_kernels.cuh), in order of preference per window:
 // usable when W == L*R exactly (LCS plots with h = 1).
 constexpr ShapeDef kDualShapes[] = {
-    {4, 32, 1}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {8, 8, 2}, {4, 16, 2},
-    {4, 32, 2}, {8, 32, 1}, {8, 16, 1}, {16, 16, 2}, {8, 8, 1},
+    {4, 32, 2}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {8, 8, 2}, {4, 16, 2},
+    {4, 32, 1}, {8, 32, 1}, {8, 16, 1}, {16, 16, 2}, {8, 8, 1},
     {4, 8, 2}, {4, 24, 2}, {8, 24, 2}, {16, 24, 2}, {32, 24, 2}, {16, 32, 2}, {32, 32, 2},
     // lane groups that do not tile the warp (30 of 32 lanes work): windows 80, 100, 120, 160, 200, 320
     // (9-33% faster than the single-pair kernel; <10,24,2> for 240 and <20,20,1> for 400 were not)
