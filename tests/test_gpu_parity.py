@@ -337,6 +337,27 @@ def test_dual_kernel_row_shards(ndev, monkeypatch):
     assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
 
 
+@pytest.mark.parametrize("w", [64, 100])
+def test_dual_kernel_tiny_plots(w, monkeypatch):
+    """Edge sizes through the dual-pair kernel: 1-5 grid rows (groups with missing strips and a
+    missing second pair), a single-column and a two-column y."""
+    monkeypatch.setenv("AP_DUAL", "1")
+    rng = np.random.default_rng(w)
+    for rows in (1, 2, 3, 4, 5):
+        for ncols in (1, 2, 37):
+            x = rng.integers(1, 5, w + rows - 1).astype(np.uint8)
+            y = np.concatenate([x[:w // 2], rng.integers(1, 5, w - w // 2 + ncols - 1)]).astype(np.uint8)
+            rc, want = ol.plot_rows(x, y, w, 1, 1)
+            assert rc == 0 and want.shape == (rows, ncols)
+            assert np.array_equal(gpu_grid(x, y, w, 1, 1), want), (rows, ncols)
+            t = int(want.max())
+            rr, cc = np.nonzero(want >= t)
+            gr, gc, gh = ap.plot_threshold_arrays(x, y, cfg(w, 1, 1), t)
+            assert np.array_equal(gr, rr) and np.array_equal(gc, cc) and np.array_equal(gh, want[rr, cc])
+    name, _ = last_kernel_name(x, y, w, 1, 1)
+    assert name.startswith("combd<"), name
+
+
 def test_dual_kernel_gate_and_streamed_blocks(monkeypatch):
     """Small plots keep the single-pair kernel (too few pair groups to fill the GPU), large ones
     take the dual-pair kernel; the streamed host plot (row blocks whose mask words reach into
