@@ -13,9 +13,10 @@
 // x-window of the pair (4g, 4g+1) shifted by two characters, so its mask word
 // of strip row i is the first pair's word of row i + 2: a lane that holds rows
 // [jR, jR+R) of BOTH pairs reads R + 2 words (R/4 LDS.128 + one LDS.64 per
-// band: the first half of the quad below it) for 4R cells instead of 2R — 1.8x fewer table wavefronts per cell, four
-// independent seaweed chains per lane (K = 2 bands x 2 pairs), and the per-step
-// overhead (shuffles, code feed, table addresses) shared by twice the cells.
+// band: the first half of the quad below it) for 4R cells instead of 2R —
+// 1.8x fewer table wavefronts per cell, four independent seaweed chains per
+// lane (K = 2 bands x 2 pairs), and the per-step overhead (shuffles, code feed,
+// table addresses) shared by twice the cells.
 //
 // One table per warp.  Group g's rows are group 0's shifted by 4g characters = g quads, so
 // all groups of a warp read one table: per code and lane index j a run of G + R/4 quads
@@ -130,11 +131,10 @@ combd_kernel(const CombParams p) {
   const uint32_t j = lane % L;
   uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][CS]: L runs of PJ quads
   const size_t tbytes = size_t(p.sigma) * CS * 16;
-  constexpr size_t xbytes = 0;
   constexpr int RSG = ring_stride(L, kChunk);
-  uint32_t* ring0 = reinterpret_cast<uint32_t*>(smem + tbytes + xbytes) + g * RSG;
+  uint32_t* ring0 = reinterpret_cast<uint32_t*>(smem + tbytes) + g * RSG;
   uint32_t* ring1 = ring0 + Ga * RSG;
-  const uint32_t okb = uint32_t(__cvta_generic_to_shared(smem + tbytes + xbytes)) +
+  const uint32_t okb = uint32_t(__cvta_generic_to_shared(smem + tbytes)) +
                        ((2 * Ga * RSG * 4 + 15) & ~15u) + g * uint32_t(ok_stride(p.ring));
   // the phantom group folds every ok slot onto its 64-byte scratch
   const uint32_t okmask = g < uint32_t(G) ? p.ring - 1 : 0u;
