@@ -99,6 +99,9 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 #ifndef AP_DUAL_MINB16
 #define AP_DUAL_MINB16 12  // same for the R = 16 shapes
 #endif
+#ifndef AP_DUAL_HF_MOD
+#define AP_DUAL_HF_MOD 4      // ... of every AP_DUAL_HF_MOD rows (1 in 4: 3, 5, 6, 8 and 3 in 8 measured slower or equal)
+#endif
 #ifndef AP_DUAL_HF_PHASE0
 #define AP_DUAL_HF_PHASE0 0   // which row of every four takes the fp16 form, pair 0 / pair 1
 #endif
@@ -266,14 +269,14 @@ combd_kernel(const CombParams p) {
               {
                 uint32_t& v = V0[b * RB + i];
                 const uint32_t d = __viaddmax_s16x2(t0, m[i], v);
-                if (((i + AP_DUAL_HF_PHASE0) & 3) < kHfRows) v = hadd2u(hsub2u(v, d), t0);
+                if (((i + AP_DUAL_HF_PHASE0) % AP_DUAL_HF_MOD) < kHfRows) v = hadd2u(hsub2u(v, d), t0);
                 else v = lop3_xor(v, t0, d);
                 t0 = d;
               }
               {
                 uint32_t& v = V1[b * RB + i];
                 const uint32_t d = __viaddmax_s16x2(t1, m[i + 2], v);
-                if (((i + AP_DUAL_HF_PHASE1) & 3) < kHfRows) v = hadd2u(hsub2u(v, d), t1);
+                if (((i + AP_DUAL_HF_PHASE1) % AP_DUAL_HF_MOD) < kHfRows) v = hadd2u(hsub2u(v, d), t1);
                 else v = lop3_xor(v, t1, d);
                 t1 = d;
               }
