@@ -30,6 +30,8 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 //  0 distinct consecutive 16 B (lane*16)       1 all lanes one address
 //  2 groups of 4 lanes share 16 B (8 distinct)  3 groups of 8 lanes share (4 distinct)
 //  4 lanes of group g (4 lanes) at g*8 + j*128 (overlapping, 8-B shifted: the shared-table layout)
+//  5-10 the dual-pair kernel's table layouts: is an LDS.128 conflict-free when every aligned
+//       group of 8 lanes (a quarter warp) covers 8 different 16-B bank groups?
 // W: 32, 64, 128-bit loads
 template <int P, int W>
 __global__ void k(uint32_t* out, long long* cyc) {
@@ -42,7 +44,14 @@ __global__ void k(uint32_t* out, long long* cyc) {
   else if (P == 1) off = 0;
   else if (P == 2) off = (lane >> 2) * 16;
   else if (P == 3) off = (lane >> 3) * 16;
-  else off = (lane >> 2) * 8 + (lane & 3) * 128;
+  else if (P == 4) off = (lane >> 2) * 8 + (lane & 3) * 128;
+  // dual-pair table layouts (ap_dual_kernels.cuh): lane (g, j) at chunk PJ * j + g
+  else if (P == 5) off = ((lane & 3) * 17 + (lane >> 2)) * 16;    // L = 4, PJ = 17
+  else if (P == 6) off = ((lane & 3) * 18 + (lane >> 2)) * 16;    // L = 4, PJ = 18
+  else if (P == 7) off = ((lane & 7) * 13 + (lane >> 3)) * 16;    // L = 8, PJ = 13
+  else if (P == 8) off = ((lane & 7) * 12 + (lane >> 3)) * 16;    // L = 8, PJ = 12 (even)
+  else if (P == 9) off = ((lane % 10) * 9 + (lane / 10 < 3 ? lane / 10 : 2)) * 16;   // L = 10, PJ = 9
+  else off = ((lane % 5) * 13 + (lane / 5 < 6 ? lane / 5 : 5)) * 16;                  // L = 5, PJ = 13
   if (W == 32) off = P == 0 ? lane * 4 : off / 4 * 4;
   const uint32_t base = uint32_t(__cvta_generic_to_shared(sm)) + off + (warp & 7) * 512;
   uint32_t acc = 0;
@@ -94,6 +103,12 @@ int main() {
     run<0, 64>("distinct", w);
     run<1, 64>("broadcast", w);
     run<4, 64>("shared table (8-B group shift)", w);
+    run<5, 128>("dual table L=4 PJ=17 (2 lanes per bank group in a quarter warp)", w);
+    run<6, 128>("dual table L=4 PJ=18", w);
+    run<7, 128>("dual table L=8 PJ=13", w);
+    run<8, 128>("dual table L=8 PJ=12 (even)", w);
+    run<9, 128>("dual table L=10 PJ=9", w);
+    run<10, 128>("dual table L=5 PJ=13", w);
     run<0, 32>("distinct", w);
     run<1, 32>("broadcast", w);
   }
