@@ -102,10 +102,9 @@ constexpr ShapeDef kDualShapes[] = {
     {4, 32, 2}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {8, 8, 2}, {4, 16, 2},
     {4, 32, 1}, {8, 32, 1}, {8, 16, 1}, {16, 16, 2}, {8, 8, 1},
     {4, 8, 2}, {4, 24, 2}, {8, 24, 2}, {16, 24, 2}, {32, 24, 2}, {16, 32, 2}, {32, 32, 2},
-    // lane groups that do not tile the warp (30 of 32 lanes work): windows 80, 100, 120, 160, 200, 300,
-    // 320 (9-33% faster than the single-pair kernel; <10,24,2> for 240, <20,20,1> for 400 and <25,20,1> for
-    // 500 were not)
-    {5, 20, 1}, {10, 20, 1}, {5, 16, 2}, {5, 24, 2}, {5, 32, 2}, {10, 32, 2}, {15, 20, 1},
+    // lane groups that do not tile the warp (30 of 32 lanes work): windows 80, 100, 120, 160, 200, 240,
+    // 300, 320 (9-33% faster than the single-pair kernel; <20,20,1> for 400 and <25,20,1> for 500 were not)
+    {5, 20, 1}, {10, 20, 1}, {5, 16, 2}, {5, 24, 2}, {5, 32, 2}, {10, 32, 2}, {15, 20, 1}, {10, 24, 2},
 };
 
 bool dual_shape_fits(uint32_t W, uint32_t sigma, bool dense, int l, int r, int k, int hf, Shape* out,

@@ -36,8 +36,8 @@ KernelFn pick_dual(int l, int r, int k, bool dense, bool hf);
 // Quads between the table runs of consecutive lane indices j.  An LDS.128 is served a quarter
 // warp (8 lanes, 128 B) at a time, so PJ is the smallest run length for which the chunks
 // PJ*j + g of every aligned group of 8 lanes fall on 8 different bank groups (PJ odd for L >= 8,
-// PJ = 2 mod 4 for L = 4, 13 for L = 5; lane groups of 10 or 20 lanes straddle the quarters and
-// keep a 2-way conflict in some of them).
+// PJ = 2 mod 4 for L = 4, 13 for L = 5; lane groups of 10, 15 or 20 lanes straddle the quarters and
+// no single stride serves them: dual_base below).
 __host__ __device__ constexpr int dual_pj_conflicts(int L, int PJ) {
   const int G = 32 / L;
   int worst = 0;
@@ -66,9 +66,29 @@ __host__ __device__ constexpr int dual_pj(int L, int R) {
   }
   return best;
 }
+// First quad of lane index j's run.  Regular layouts: j * PJ.  Lane groups of 10 and 15 lanes
+// straddle the quarter warps, and no single stride is conflict-free for them (an LDS.128 cost 7
+// cycles instead of 4 with the best one, tools/lds_peak.cu); a search over the runs' bank groups
+// (base mod 8, every quarter warp all-different) gives the residues below, and each run starts at
+// the first quad with its residue after the previous run.
+__host__ __device__ constexpr int dual_base(int L, int R, int j) {
+  if (L != 10 && L != 15) return j * dual_pj(L, R);
+  constexpr int b10[10] = {0, 1, 4, 7, 2, 5, 3, 6, 4, 7};
+  constexpr int b15[15] = {0, 1, 2, 3, 4, 5, 6, 7, 0, 2, 3, 4, 5, 6, 7};
+  const int need = 32 / L + R / 4 + 1;
+  int base = 0;
+  for (int i = 1; i <= j; ++i) {
+    const int want = L == 10 ? b10[i] : b15[i];
+    base += need;
+    base += (want - base % 8 + 8) % 8;
+  }
+  return base;
+}
 // table quads per code: the L runs, rounded up to 8 quads (128 B) so that lanes holding different
 // codes (lane j is at column s - j*K - b) keep their bank group
-__host__ __device__ constexpr int dual_cs(int L, int R) { return (L * dual_pj(L, R) + 7) / 8 * 8; }
+__host__ __device__ constexpr int dual_cs(int L, int R) {
+  return (dual_base(L, R, L - 1) + 32 / L + R / 4 + 1 + 7) / 8 * 8;
+}
 
 // Shared memory per warp (one-warp CTAs): the mask table [sigma][CS] quads, two bottom-key rings
 // per group, one ok-flag ring per group; lane groups that do not tile the warp (L = 5, 10, 20)
@@ -126,13 +146,12 @@ combd_kernel(const CombParams p) {
   constexpr int RB = R / K;
   constexpr int QB = RB / 4;
   constexpr int VB = L * K;
-  constexpr int PJ = dual_pj(L, R);
   extern __shared__ __align__(16) unsigned char smem[];
 
   const uint32_t lane = lane_id();
   const uint32_t g = lane / L;
   const uint32_t j = lane % L;
-  uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][CS]: L runs of PJ quads
+  uint4* tbl = reinterpret_cast<uint4*>(smem);                        // [sigma][CS]: L runs of quads (dual_base)
   const size_t tbytes = size_t(p.sigma) * CS * 16;
   constexpr int RSG = ring_stride(L, kChunk);
   uint32_t* ring0 = reinterpret_cast<uint32_t*>(smem + tbytes) + g * RSG;
@@ -196,14 +215,14 @@ combd_kernel(const CombParams p) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             wv[k] = (xc[k] == a ? 0x00008000u : 0u) | (xc[k + 1] == a ? 0x80000000u : 0u);
-          tbl[a * CS + jj * PJ + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          tbl[a * CS + dual_base(L, R, int(jj)) + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
       for (uint32_t k = j; k <= okmask; k += L) sts_u32(okb + 4 * k, 0u);
     }
     __syncwarp();
 
-    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + j * PJ + (real_g ? g : uint32_t(G - 1))));
+    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + dual_base(L, R, int(j)) + (real_g ? g : uint32_t(G - 1))));
     const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
     const uint32_t nz = j != 0 ? 1u : 0u;
     const uint32_t finc = j == 0 ? 0x00010001u : 0u;

@@ -211,7 +211,7 @@ def test_forced_generic_shapes(shape, monkeypatch):
 DUAL_SHAPES = ["4,32,1", "4,32,2", "8,32,1", "8,32,2", "8,16,1", "8,16,2", "16,16,1", "16,16,2", "8,8,1", "8,8,2",
                "4,16,2", "4,8,2", "4,24,2", "8,24,2", "16,24,2", "32,24,2", "16,32,2", "32,32,2",
                # lane groups that do not tile the warp (idle phantom group)
-               "5,20,1", "10,20,1", "5,16,2", "5,24,2", "5,32,2", "10,32,2", "15,20,1"]
+               "5,20,1", "10,20,1", "5,16,2", "5,24,2", "5,32,2", "10,32,2", "15,20,1", "10,24,2"]
 
 
 def _dual_hf_ok(s):   # fp16 keys need W + L*K <= 768 (kHfMaxSpan)

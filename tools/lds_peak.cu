@@ -51,7 +51,11 @@ __global__ void k(uint32_t* out, long long* cyc) {
   else if (P == 7) off = ((lane & 7) * 13 + (lane >> 3)) * 16;    // L = 8, PJ = 13
   else if (P == 8) off = ((lane & 7) * 12 + (lane >> 3)) * 16;    // L = 8, PJ = 12 (even)
   else if (P == 9) off = ((lane % 10) * 9 + (lane / 10 < 3 ? lane / 10 : 2)) * 16;   // L = 10, PJ = 9
-  else off = ((lane % 5) * 13 + (lane / 5 < 6 ? lane / 5 : 5)) * 16;                  // L = 5, PJ = 13
+  else if (P == 10) off = ((lane % 5) * 13 + (lane / 5 < 6 ? lane / 5 : 5)) * 16;    // L = 5, PJ = 13
+  else {   // L = 10, R = 20 with per-run bank residues (dual_base): runs at quads 0, 9, 20, 31, 42, 53, 67, 78, 92, 103
+    const int base[10] = {0, 9, 20, 31, 42, 53, 67, 78, 92, 103};
+    off = (base[lane % 10] + (lane / 10 < 3 ? lane / 10 : 2)) * 16;
+  }
   if (W == 32) off = P == 0 ? lane * 4 : off / 4 * 4;
   const uint32_t base = uint32_t(__cvta_generic_to_shared(sm)) + off + (warp & 7) * 512;
   uint32_t acc = 0;
@@ -109,6 +113,7 @@ int main() {
     run<8, 128>("dual table L=8 PJ=12 (even)", w);
     run<9, 128>("dual table L=10 PJ=9", w);
     run<10, 128>("dual table L=5 PJ=13", w);
+    run<11, 128>("dual table L=10, runs placed by bank residue", w);
     run<0, 32>("distinct", w);
     run<1, 32>("broadcast", w);
   }

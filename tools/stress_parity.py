@@ -38,7 +38,7 @@ def main():
         r = 1 + int(rng.integers(0, 2))
         if args.dual:
             r, h = 1, 1
-            w = int(rng.choice([32, 64, 64, 80, 96, 100, 100, 120, 128, 128, 160, 192, 200, 256, 256, 300, 320, 384, 512,
+            w = int(rng.choice([32, 64, 64, 80, 96, 100, 100, 120, 128, 128, 160, 192, 200, 240, 256, 256, 300, 320, 384, 512,
                                768, 1024]))
             sigma = int(rng.choice([2, 4, 4, 20, 60]))
             m = int(rng.integers(w, w + 300))
