@@ -84,6 +84,17 @@ __host__ __device__ constexpr int dual_base(int L, int R, int j) {
   }
   return base;
 }
+// the same for a run-time lane index inside the kernels: the regular stride is folded at compile
+// time (dual_pj's search must not run per task)
+template <int L, int R>
+__device__ __forceinline__ uint32_t dual_base_rt(uint32_t j) {
+  if constexpr (L == 10 || L == 15) {
+    return uint32_t(dual_base(L, R, int(j)));
+  } else {
+    constexpr int kPj = dual_pj(L, R);
+    return j * uint32_t(kPj);
+  }
+}
 // table quads per code: the L runs, rounded up to 8 quads (128 B) so that lanes holding different
 // codes (lane j is at column s - j*K - b) keep their bank group
 __host__ __device__ constexpr int dual_cs(int L, int R) {
@@ -199,6 +210,7 @@ combd_kernel(const CombParams p) {
       const uint32_t rw = 4 * pg * G;   // h = 1: strip s starts at x[s]
       for (uint32_t e = lane; e < uint32_t(L * (G + Q)); e += 32) {
         const uint32_t jj = e / (G + Q), c = e % (G + Q);
+        const uint32_t jbase = dual_base_rt<L, R>(jj);
         uint32_t xc[5];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
@@ -215,14 +227,14 @@ combd_kernel(const CombParams p) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             wv[k] = (xc[k] == a ? 0x00008000u : 0u) | (xc[k + 1] == a ? 0x80000000u : 0u);
-          tbl[a * CS + dual_base(L, R, int(jj)) + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          tbl[a * CS + jbase + c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
       for (uint32_t k = j; k <= okmask; k += L) sts_u32(okb + 4 * k, 0u);
     }
     __syncwarp();
 
-    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + dual_base(L, R, int(j)) + (real_g ? g : uint32_t(G - 1))));
+    const uint32_t tlb = uint32_t(__cvta_generic_to_shared(tbl + dual_base_rt<L, R>(j) + (real_g ? g : uint32_t(G - 1))));
     const uint4* yq = reinterpret_cast<const uint4*>((j == 0 ? p.ycol : p.ycol_zero) + c0);
     const uint32_t nz = j != 0 ? 1u : 0u;
     const uint32_t finc = j == 0 ? 0x00010001u : 0u;
