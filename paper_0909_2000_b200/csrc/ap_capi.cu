@@ -99,7 +99,7 @@ struct Shape {
 // Dual-pair shapes (combd_kernel, ap_dual_kernels.cuh), in order of preference per window:
 // usable when W == L*R exactly (LCS plots with h = 1).
 constexpr ShapeDef kDualShapes[] = {
-    {4, 32, 2}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {8, 8, 2}, {4, 16, 2},
+    {4, 32, 2}, {8, 32, 2}, {8, 16, 2}, {16, 16, 1}, {4, 16, 2}, {8, 8, 2},
     {4, 32, 1}, {8, 32, 1}, {8, 16, 1}, {16, 16, 2}, {8, 8, 1},
     {4, 8, 2}, {4, 24, 2}, {8, 24, 2}, {16, 24, 2}, {32, 24, 2}, {16, 32, 2}, {32, 32, 2},
     // lane groups that do not tile the warp (30 of 32 lanes work): windows 80, 100, 120, 160, 200, 240,
@@ -146,10 +146,13 @@ bool choose_shape(uint32_t W, uint32_t sigma, bool dense, Shape* out, bool dual_
     // ~90 KB per warp the single-pair kernel wins (sigma = 120, w = 64: 10.5 against 13.4-16.4)
     for (const ShapeDef& d : kDualShapes)
       if (dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out, kSmemPerSm / 8 - 1024)) return true;
-    for (int pass = 0; pass < 2; ++pass)
-      for (const ShapeDef& d : kDualShapes)
-        if ((d.K == 2) == (pass == 0) && dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out, 90 * 1024))
-          return true;
+    // (among those the 8-lane groups measured best: sigma = 60, w = 64: <8,8,2> 8.6 ms, <4,16,2> 9.6;
+    // sigma = 20, w = 256: <8,32,2> 20.4, <16,16,2> 22.1)
+    for (int pass = 0; pass < 3; ++pass)
+      for (const ShapeDef& d : kDualShapes) {
+        const int cls = d.K == 2 ? (d.L == 8 ? 0 : 1) : 2;
+        if (cls == pass && dual_shape_fits(W, sigma, dense, d.L, d.R, d.K, -1, out, 90 * 1024)) return true;
+      }
   }
   out->dual = false;
   double best = 1e30;
